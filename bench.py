@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: TT-circuit TFIM energy+gradient evaluations per second on B200.
+
+Default workload (N=1): BASELINE.json configs[1] = cfg2: TTCircuit n=100, 10 layers
+(5 RotY rows + 5 CZ lines, reading A), TFIM energy + full gradient, 256 parameter
+sets per step.  ``--config cfg4`` (n=1000, 20 layers, chain sharded over ranks) and
+``--config cfg5`` (n=1024 per GPU, forward only, weak scaling) are also available.
+
+One JSON line on rank 0 (contract in the task brief): value = whole-job evals/s from
+device-resident inputs; e2e = same metric through ExpvalProgram with pinned host
+buffers (H2D + D2H inside the timed region); roofline for the dominant sweep kernel
+against the measured FP32 FFMA peak; cpu_baseline = the CPU oracle port of the
+reference timed on this host.  ``--impl reference`` times that CPU path alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "expectation+gradient evals/sec at n qubits, L layers (1/2/4/8 B200); HBM GB/s frac"
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc, self.thread = index, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return None
+        loaded = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for _, _, r in loaded:
+            for bit, name in REASON_BITS.items():
+                if r & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in loaded), "sm_max_mhz": max(s[1] for s in loaded),
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def _oracle_eval(args):
+    n, layers, rot, ent, theta = args
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    import oracle as O
+
+    c = O.ry_cz_layers(n, layers, rot, ent)
+    t0 = time.perf_counter()
+    O.grad_expval_tt(c, O.tfim_terms(n), theta)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_rate(cfg, thetas, workers):
+    """Evaluate theta-sets with the CPU oracle port on `workers` processes; returns evals/s."""
+    import multiprocessing as mp
+
+    jobs = [(cfg.n, cfg.layers, cfg.rot, cfg.ent, th) for th in thetas]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        pool.map(_oracle_eval, jobs[:workers])  # warm the workers (imports)
+        t0 = time.perf_counter()
+        per = pool.map(_oracle_eval, jobs)
+        wall = time.perf_counter() - t0
+    return len(jobs) / wall, wall, float(sum(per))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2112_10239_b200.workloads import theta_sets
+
+    cores = host_cores()
+    per_step = max(cores, 4)
+    thetas = theta_sets(cfg.circuit().n_params, per_step * (args.steps + args.warmup), seed=0)
+    import multiprocessing as mp
+
+    jobs = [(cfg.n, cfg.layers, cfg.rot, cfg.ent, th) for th in thetas]
+    with mp.get_context("fork").Pool(cores) as pool:
+        for w in range(args.warmup):
+            pool.map(_oracle_eval, jobs[w * per_step:(w + 1) * per_step])
+        t0 = time.perf_counter()
+        off = args.warmup * per_step
+        for s in range(args.steps):
+            pool.map(_oracle_eval, jobs[off + s * per_step: off + (s + 1) * per_step])
+        wall = time.perf_counter() - t0
+    value = args.steps * per_step / wall
+    sample = f"{per_step} theta-sets of {cfg.name} per step (CPU oracle port of tnsim grad_expval(engine='tt', eps=0))"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded U[-pi,pi) angles, float32-rounded)",
+        "config": config_block(cfg, None, per_step),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, plan, batch, n_override=None, world=1):
+    n = n_override or cfg.n
+    blk = {"workload": f"{cfg.name}: {cfg.description}", "n_qubits": n, "layers": cfg.layers,
+           "rotation_rows": (cfg.layers + 1) // 2, "entangler_lines": cfg.layers // 2,
+           "rotation": cfg.rot, "entangler": cfg.ent, "operator": "TFIM open chain j=h=1",
+           "batch_per_gpu": batch, "gradient": cfg.grad,
+           "layer_semantics": "reading A (layer = one TTCircuit unitary)"}
+    if plan is not None:
+        blk.update({"segments": plan.n_segments, "chi_max": plan.chi_max, "mpo_channels": plan.d_max,
+                    "sub_chain_sites": int(plan.info.get("sub_chain_sites", 0))})
+    blk["parallelism"] = ("theta-set data parallel" if cfg.name in ("cfg1", "cfg2") else "qubit-chain segments") + (
+        f" over {world} GPUs" if world > 1 else "")
+    return blk
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2112_10239_b200 import _lib, engine as E
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200 import roofline
+    from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, tfim
+    from paper_2112_10239_b200.program import ExpvalProgram
+    from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
+
+    batch = args.batch or cfg.batch
+    sharded = cfg.name in ("cfg4", "cfg5")
+    n = cfg.n * ws if cfg.name == "cfg5" else cfg.n
+    circuit = layered_circuit(n, cfg.layers, cfg.rot, cfg.ent)
+    ham_full = tfim(n)
+    if sharded and ws > 1:
+        lo, hi = rank * n // ws, (rank + 1) * n // ws
+        ham = PauliHamiltonian(n, tuple(t for t in ham_full.terms if lo <= t.support[0] < hi))
+    else:
+        ham = ham_full
+    seed = 0 if sharded else rank
+    thetas = theta_sets(circuit.n_params, batch, seed=seed)
+    prog = ExpvalProgram(circuit, ham, batch, device=dev, segments=args.segments, grad=cfg.grad)
+    plan = prog.plan
+    theta_dev = torch.tensor(thetas, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    lib = _lib.load()
+    import ctypes
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    code = _lib.TQ_C64
+    ws_buf, ws_bytes = prog.dp.workspace(batch, _lib.TQ_FLAG_GRAD if cfg.grad else 0, code, stream.cuda_stream)
+    energy = torch.empty(batch, 2, dtype=torch.float64, device=dev)
+    grad = torch.empty(batch, circuit.n_params, dtype=torch.float32, device=dev) if cfg.grad else None
+    ms_k = (ctypes.c_float * 2)()
+
+    def step(timed=False):
+        fn = lib.tq_energy_grad_timed if timed else lib.tq_energy_grad
+        extra = (ms_k,) if timed else ()
+        st = fn(ctypes.byref(prog.dp.chain), code, batch, theta_dev.data_ptr(), theta_dev.stride(0),
+                prog.coef.data_ptr(), 0, energy.data_ptr(), grad.data_ptr() if grad is not None else None,
+                ws_buf.data_ptr(), ws_bytes, stream.cuda_stream, *extra)
+        _lib.check(st)
+        if ws > 1 and sharded:
+            import torch.distributed as dist
+
+            dist.all_reduce(energy)
+            if grad is not None:
+                dist.all_reduce(grad)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard inside the bench: finite outputs
+    E.check_finite(energy, grad)
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.25)
+    step_ms, rl_ms, lr_ms = [], [], []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2); not timed
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(timed=True)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        rl_ms.append(ms_k[0])
+        lr_ms.append(ms_k[1])
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    tot = sum(step_ms)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t)
+    ms_per_step = tot / args.steps
+    evals_per_step = batch * (ws if not sharded else 1)
+    value = evals_per_step / (ms_per_step * 1e-3)
+
+    # ---- e2e through the host-buffer entry (pinned host -> device -> host)
+    host = torch.tensor(thetas, dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        prog(host, copy_out=False)
+    e2e_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        prog(host, copy_out=False)
+        if ws > 1 and sharded:
+            import torch.distributed as dist
+
+            dist.all_reduce(prog.e_host.to(dev))
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    barrier()
+    e2e_tot = sum(e2e_ms)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t)
+    e2e_value = evals_per_step / (e2e_tot / args.steps * 1e-3)
+
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant sweep against the measured FFMA peak
+    plan1 = C.compile_chain(circuit, C.normalize_terms(ham), "energy", batch=batch, segments=1)
+    model = roofline.eval_model(plan1, grad=cfg.grad)
+    ffma = ctypes.c_double(0)
+    _lib.check(lib.tq_ffma_peak(20000, stream.cuda_stream, ctypes.byref(ffma)))
+    peak_fp32 = ffma.value
+    mean_rl = statistics.mean(rl_ms)
+    mean_lr = statistics.mean(lr_ms) if cfg.grad else 0.0
+    if mean_lr >= mean_rl:
+        kname, kms, kflops = "lr_sweep (gradient)", mean_lr, model["flops_lr"] * batch
+    else:
+        kname, kms, kflops = "rl_sweep (energy)", mean_rl, model["flops_rl"] * batch
+    achieved = kflops / (kms * 1e-3) / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    step_bytes = model["bytes"] * batch
+    hbm_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get(kname.split()[0])
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cores = host_cores()
+        sample_n = min(256, max(2 * cores, 16))
+        rate, wall, cpu_s = cpu_oracle_rate(cfg, theta_sets(circuit.n_params, sample_n, seed=99), cores)
+        cpu = {"value": rate, "unit": "evals/s", "cores": cores, "kind": "port",
+               "sample": f"{sample_n} theta-sets of {cfg.name} (oracle port of tnsim grad_expval engine='tt' eps=0), "
+                         f"{cpu_s:.1f} CPU-s over {wall:.1f} s wall"}
+
+    launches_per_step = 2 + (2 if cfg.grad else 0)  # rl_sweep+reduce_energy (+ lr_sweep+reduce_grad)
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic (seeded U[-pi,pi) angles, float32-rounded; random-init circuit of the named architecture)",
+        "config": {**config_block(cfg, plan, batch, n, ws),
+                   "l2": "flushed between timed steps (256 MiB memset, untimed)"},
+        "roofline": {"bound": "fp32_simt", "kernel": kname, "achieved": achieved, "peak": peak_fp32,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fp32 if peak_fp32 else None, "traffic": traffic,
+                     "peak_source": "measured FFMA probe (tq_ffma_peak) on this GPU in this run",
+                     "flops_per_launch": kflops, "kernel_ms": kms,
+                     "rl_ms": mean_rl, "lr_ms": mean_lr},
+        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
+                "bytes_per_step": step_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": prog.h2d_bytes,
+                "d2h_bytes_per_step": prog.d2h_bytes, "ms_per_step": e2e_tot / args.steps},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--segments", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2112_10239_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

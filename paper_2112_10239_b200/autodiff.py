@@ -1,0 +1,286 @@
+"""Reference-compatible value/gradient API on the B200 engine.
+
+Same names, argument meaning and error behaviour as ``tnsim.autodiff``
+(reference ``autodiff.py:445-659``) for the TT engine.  Differences:
+
+* ``engine`` accepts ``"tt"`` / ``"b200"`` (both mean this engine); the reference's
+  ``"dense"`` oracle engine is not part of the product and raises ``InputError``.
+* The engine is exact (the reference's ``eps=0`` semantics) for any ``eps``;
+  ``chi_max`` below the exact factored bond raises ``InputError`` (truncated
+  straight-through mode is a later row).
+* ``theta`` may be 2-D ``[B, P]``: B independent parameter sets in one launch.
+* ``dtype="complex64"`` (default, the B200 fast path) or ``"complex128"`` (parity mode).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import chain as C
+from . import engine as E
+from .circuits import Circuit
+from .errors import (
+    DivergenceDetected,
+    InputError,
+    ParamCountMismatch,
+    UnsupportedGateForShift,
+    WireOutOfRange,
+)
+from .hamiltonians import PAULI_MATRICES, PauliHamiltonian
+
+SHIFTABLE_GATES = ("rx", "ry", "rz", "crz")
+_CRZ_Y1 = (np.sqrt(2.0) + 1.0) / (4.0 * np.sqrt(2.0))
+_CRZ_Y2 = (np.sqrt(2.0) - 1.0) / (4.0 * np.sqrt(2.0))
+
+
+def _check_engine(engine: str) -> str:
+    """Reference autodiff.py:456-459 (engine seam)."""
+    if engine in ("tt", "b200"):
+        return engine
+    if engine == "dense":
+        raise InputError("engine 'dense' is the reference's CPU oracle and is not part of the B200 engine")
+    raise InputError(f"unknown engine {engine!r}; expected 'tt' or 'b200'")
+
+
+def _check_theta(circuit: Circuit, theta):
+    """Reference autodiff.py:445-453; returns float64 [B, P] and whether input was 1-D."""
+    if isinstance(theta, torch.Tensor):
+        theta = theta.detach().cpu().double().numpy()
+    arr = np.asarray(theta, dtype=float)
+    single = arr.ndim <= 1
+    arr = arr.reshape(1, -1) if single else arr
+    if arr.ndim != 2 or arr.shape[1] != circuit.n_params:
+        raise ParamCountMismatch(f"{arr.shape[-1] if arr.ndim else arr.size} parameters supplied, "
+                                 f"circuit has {circuit.n_params} slots")
+    if arr.size and not np.all(np.isfinite(arr)):
+        raise InputError("parameters must be finite")
+    return arr, single
+
+
+def _check_chi(plan, chi_max):
+    if chi_max is not None and int(chi_max) < plan.chi_max:
+        raise InputError(f"chi_max={chi_max} would truncate the exact factored bond {plan.chi_max}; "
+                         "the B200 engine is exact (eps=0 semantics)")
+
+
+def _device(device):
+    if device is None:
+        if not torch.cuda.is_available():
+            from .errors import EngineUnavailable
+            raise EngineUnavailable("no CUDA device is available; the B200 engine has no CPU fallback")
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _terms(ham: PauliHamiltonian, n: int):
+    if ham.n_qubits != n:
+        raise InputError(f"state has {n} qubits, Hamiltonian {ham.n_qubits}")
+    return C.normalize_terms(ham)
+
+
+def energy(circuit: Circuit, ham: PauliHamiltonian, theta: torch.Tensor, *, dtype: str = "complex64",
+           segments=None, check: bool = True) -> torch.Tensor:
+    """Torch-native, differentiable: theta [B,P] (device tensor) -> Re<H> [B] (float64).
+
+    Gradients are produced by the same engine call (the reference's one-tape
+    value+gradient, autodiff.py:471-487) and flow through ``torch.autograd``."""
+    terms = _terms(ham, circuit.n_qubits)
+    if theta.dim() == 1:
+        theta = theta[None]
+    dev = theta.device
+    dp = E.device_plan(circuit, terms, "energy", theta.shape[0], dev, segments, dtype=dtype)
+    coef = torch.tensor([[c.real for c, _ in terms]], dtype=torch.float64, device=dev)
+    val, full = E.ExpvalFunction.apply(theta, dp, coef, dtype)
+    if check:
+        E.check_finite(full)
+        im_extra = None
+        if any(c.imag != 0 for c, _ in terms):
+            cim = torch.tensor([[c.imag for c, _ in terms]], dtype=torch.float64, device=dev)
+            e_im, _ = E.energy_grad_raw(dp, theta.detach(), cim, False, dtype)
+            im_extra = e_im[:, 0]
+        E.check_residue(full, im_extra, E.residue_tol(dtype, sum(abs(c) for c, _ in terms)))
+    return val
+
+
+def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "tt", eps: float = 0.0,
+                chi_max=None, *, dtype: str = "complex64", device=None, segments=None):
+    """Value and gradient of <H> (reference autodiff.py:471-487).
+
+    1-D theta -> (float, float64[P]); 2-D theta [B,P] -> (float64[B], float64[B,P])."""
+    _check_engine(engine)
+    arr, single = _check_theta(circuit, theta)
+    dev = _device(device)
+    terms = _terms(ham, circuit.n_qubits)
+    dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)
+    _check_chi(dp.plan, chi_max)
+    tdt = E.DTYPES[dtype][1]
+    th = torch.tensor(arr, dtype=tdt, device=dev, requires_grad=True)
+    val = energy(circuit, ham, th, dtype=dtype, segments=segments)
+    (g,) = torch.autograd.grad(val.sum(), th)
+    v = val.detach().cpu().numpy()
+    gg = g.detach().double().cpu().numpy()
+    if single:
+        return float(v[0]), gg[0]
+    return v, gg
+
+
+def evaluate_expval(circuit: Circuit, ham: PauliHamiltonian, theta=None, engine: str = "tt", eps: float = 0.0,
+                    chi_max=None, *, dtype: str = "complex64", device=None, segments=None):
+    """Forward-only <H> (reference autodiff.py:490-503): one right-to-left sweep, nothing stored."""
+    _check_engine(engine)
+    arr, single = _check_theta(circuit, circuit.params() if theta is None else theta)
+    dev = _device(device)
+    terms = _terms(ham, circuit.n_qubits)
+    dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)
+    _check_chi(dp.plan, chi_max)
+    th = torch.tensor(arr, dtype=E.DTYPES[dtype][1], device=dev)
+    v = energy(circuit, ham, th, dtype=dtype, segments=segments).cpu().numpy()
+    return float(v[0]) if single else v
+
+
+def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", *, dtype: str = "complex64",
+                       device=None, segments=None):
+    """Complex <P> per op-group sharing one state per theta-set (the values of
+    reference taped_expectations, autodiff.py:405-425).  op_groups: dicts {qubit: letter}."""
+    _check_engine(engine)
+    arr, single = _check_theta(circuit, theta)
+    n = circuit.n_qubits
+    from .hamiltonians import PauliTerm
+
+    terms = []
+    for ops in op_groups:
+        for q, letter in dict(ops).items():
+            if letter not in PAULI_MATRICES:
+                raise InputError(f"unknown Pauli letter {letter!r}")
+            if not 0 <= int(q) < n:
+                raise WireOutOfRange(f"qubit {q} outside 0..{n - 1}")
+        terms.append(PauliTerm(1.0, tuple(dict(ops).items())))
+    ham_terms = C.normalize_terms(PauliHamiltonian(n, tuple(terms)))
+    dev = _device(device)
+    dp = E.device_plan(circuit, ham_terms, "values", arr.shape[0], dev, segments, dtype=dtype)
+    th = torch.tensor(arr, dtype=E.DTYPES[dtype][1], device=dev)
+    vals = E.values_raw(dp, th, dtype).cpu().numpy()
+    return vals[0] if single else vals
+
+
+def parameter_shift_grad(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "tt", eps: float = 0.0,
+                         chi_max=None, *, coords=None, dtype: str = "complex64", device=None):
+    """Exact shift-rule gradient (reference autodiff.py:514-550), all shifted angle
+    sets evaluated in ONE batched forward launch."""
+    _check_engine(engine)
+    arr, _ = _check_theta(circuit, theta)
+    th = arr[0]
+    names = [circuit.gates[g].name for g in circuit.trainable]
+    for name in names:
+        if name not in SHIFTABLE_GATES:
+            raise UnsupportedGateForShift(f"no shift rule for gate {name!r}")
+    ks = list(range(len(th))) if coords is None else [int(k) for k in coords]
+    rows, plan_rows = [], []
+    for k in ks:
+        shifts = (np.pi / 2, -np.pi / 2, 3 * np.pi / 2, -3 * np.pi / 2) if names[k] == "crz" else (np.pi / 2, -np.pi / 2)
+        idx = []
+        for d in shifts:
+            t = th.copy()
+            t[k] += d
+            idx.append(len(rows))
+            rows.append(t)
+        plan_rows.append((k, idx))
+    grad = np.zeros(len(th))
+    if not rows:
+        return grad
+    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), dtype=dtype, device=device))
+    for k, idx in plan_rows:
+        if names[k] == "crz":
+            grad[k] = _CRZ_Y1 * (e[idx[0]] - e[idx[1]]) - _CRZ_Y2 * (e[idx[2]] - e[idx[3]])
+        else:
+            grad[k] = 0.5 * (e[idx[0]] - e[idx[1]])
+    return grad
+
+
+def finite_diff_grad(circuit: Circuit, ham: PauliHamiltonian, theta, step: float = 1e-5, engine: str = "tt",
+                     eps: float = 0.0, chi_max=None, *, dtype: str = "complex128", device=None):
+    """Central differences (reference autodiff.py:553-576), batched into one launch."""
+    if step <= 0:
+        raise InputError(f"step must be positive, got {step}")
+    arr, _ = _check_theta(circuit, theta)
+    th = arr[0]
+    rows = []
+    for k in range(len(th)):
+        up, dn = th.copy(), th.copy()
+        up[k] += step
+        dn[k] -= step
+        rows += [up, dn]
+    if not rows:
+        return np.zeros(0)
+    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), dtype=dtype, device=device))
+    return (e[0::2] - e[1::2]) / (2 * step)
+
+
+# --------------------------------------------------------------------------- optimisation
+@dataclass(frozen=True)
+class MinimizeStep:
+    iteration: int
+    theta: np.ndarray
+    value: float
+    grad_norm: float
+
+
+@dataclass(frozen=True)
+class MinimizeResult:
+    steps: tuple
+    converged: bool
+
+    @property
+    def theta(self):
+        return self.steps[-1].theta
+
+    @property
+    def value(self):
+        return self.steps[-1].value
+
+    @property
+    def n_iters(self):
+        return self.steps[-1].iteration
+
+
+def init_params(n_params: int, rng) -> np.ndarray:
+    """Uniform angles in [-pi, pi) (reference autodiff.py:609-611)."""
+    return rng.uniform(-np.pi, np.pi, size=int(n_params))
+
+
+def minimize(fun, theta0, optimizer: str = "gd", rate: float = 0.05, max_iters: int = 200, tol: float = 1e-8,
+             betas=(0.9, 0.999), adam_eps: float = 1e-8) -> MinimizeResult:
+    """Fixed-rate descent on fun(theta) -> (value, grad) (reference autodiff.py:614-659)."""
+    if optimizer not in ("gd", "adam"):
+        raise InputError(f"unknown optimizer {optimizer!r}")
+    theta = np.asarray(theta0, dtype=float).reshape(-1).copy()
+    if theta.size and not np.all(np.isfinite(theta)):
+        raise InputError("initial parameters must be finite")
+    steps = []
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    for it in range(max_iters + 1):
+        value, grad = fun(theta)
+        value = float(value)
+        grad = np.asarray(grad, dtype=float).reshape(-1)
+        if not np.isfinite(value) or not np.all(np.isfinite(grad)):
+            raise DivergenceDetected(f"non-finite objective at iteration {it}")
+        gnorm = float(np.linalg.norm(grad))
+        steps.append(MinimizeStep(it, theta.copy(), value, gnorm))
+        if gnorm < tol:
+            return MinimizeResult(tuple(steps), True)
+        if it == max_iters:
+            break
+        if optimizer == "gd":
+            theta = theta - rate * grad
+        else:
+            b1, b2 = betas
+            m = b1 * m + (1 - b1) * grad
+            v = b2 * v + (1 - b2) * grad * grad
+            mhat = m / (1 - b1 ** (it + 1))
+            vhat = v / (1 - b2 ** (it + 1))
+            theta = theta - rate * mhat / (np.sqrt(vhat) + adam_eps)
+    return MinimizeResult(tuple(steps), False)

@@ -163,6 +163,9 @@ class Circuit:
 
     def structure_key(self):
         """Hashable key of everything except trainable parameter values (for plan caching)."""
+        cached = self.__dict__.get("_skey")
+        if cached is not None:
+            return cached
         tr = set(self.trainable)
         parts = []
         for i, g in enumerate(self.gates):
@@ -170,7 +173,9 @@ class Circuit:
                 parts.append((g.name, g.wires, "T"))
             else:
                 parts.append((g.name, g.wires, g.matrix.tobytes()))
-        return (self.n_qubits, tuple(parts), self.trainable)
+        key = (self.n_qubits, tuple(parts), self.trainable)
+        object.__setattr__(self, "_skey", key)
+        return key
 
 
 def with_params(circuit: Circuit, theta) -> Circuit:

@@ -1,0 +1,71 @@
+"""Prepared batched evaluation (serving path): compile once, evaluate many angle batches.
+
+``ExpvalProgram(circuit, ham, batch)(theta_host)`` is the host-buffer entry a
+service calls: pinned host angles -> device, one engine launch pair, energies
+and gradients back to pinned host memory.  It is what ``bench.py`` times for the
+end-to-end (``e2e``) number.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import chain as C
+from . import engine as E
+from .errors import InputError
+
+
+class ExpvalProgram:
+    def __init__(self, circuit, ham, batch: int, *, dtype: str = "complex64", device=None, segments=None,
+                 grad: bool = True):
+        self.circuit, self.ham, self.batch, self.dtype, self.grad = circuit, ham, int(batch), dtype, grad
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.terms = C.normalize_terms(ham)
+        self.dp = E.device_plan(circuit, self.terms, "energy", self.batch, self.device, segments, dtype=dtype)
+        tdt = E.DTYPES[dtype][1]
+        P = circuit.n_params
+        self.coef = torch.tensor([[c.real for c, _ in self.terms]], dtype=tdt, device=self.device)
+        self.theta_dev = torch.empty(self.batch, P, dtype=tdt, device=self.device)
+        self.theta_host = torch.empty(self.batch, P, dtype=tdt, pin_memory=True)
+        self.e_host = torch.empty(self.batch, 2, dtype=torch.float64, pin_memory=True)
+        self.g_host = torch.empty(self.batch, P, dtype=tdt, pin_memory=True) if grad else None
+
+    @property
+    def plan(self):
+        return self.dp.plan
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.theta_host.numel() * self.theta_host.element_size()
+
+    @property
+    def d2h_bytes(self) -> int:
+        n = self.e_host.numel() * self.e_host.element_size()
+        if self.g_host is not None:
+            n += self.g_host.numel() * self.g_host.element_size()
+        return n
+
+    def run_device(self, theta_dev: torch.Tensor):
+        """Device-resident inputs -> device outputs (no host traffic)."""
+        return E.energy_grad_raw(self.dp, theta_dev, self.coef, self.grad, self.dtype)
+
+    def __call__(self, theta, copy_out: bool = True):
+        """theta: [batch, P] host array (numpy or pinned torch). Returns (E[B], grad[B,P] | None)."""
+        if isinstance(theta, np.ndarray):
+            if theta.shape != tuple(self.theta_host.shape):
+                raise InputError(f"theta must be {tuple(self.theta_host.shape)}")
+            self.theta_host.numpy()[...] = theta
+            src = self.theta_host
+        else:
+            src = theta
+        self.theta_dev.copy_(src, non_blocking=True)
+        energy, grad = self.run_device(self.theta_dev)
+        self.e_host.copy_(energy, non_blocking=True)
+        if grad is not None:
+            self.g_host.copy_(grad, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if not copy_out:
+            return self.e_host, self.g_host
+        e = self.e_host[:, 0].numpy().copy()
+        return e, (self.g_host.numpy().copy() if grad is not None else None)

@@ -1,0 +1,52 @@
+"""Algorithmic work model of the engine's sweeps (DESIGN.md section "Roofline").
+
+Counts complex multiply-adds (cMAC, 8 real flops each) exactly as the kernels issue
+them for an UNSEGMENTED chain (segments=1), so light-cone halo redundancy never
+inflates ``achieved``:
+
+  fold        chi_l*chi_r pairs x ops x 4 cMAC                       (both sweeps)
+  RL          N: 2*Db*chi_l*chi_r^2     P: 2*Da*chi_l^2*chi_r
+  LR          M: 2*Da*chi_l^2*chi_r     Lam: 2*Db*chi_r^2*chi_l     G: 2*Db*chi_l*chi_r^2
+  adjoint     chi_l*chi_r pairs x ops x 12 cMAC (u and v walks + sigma contraction)
+  brackets    2*D*chi_l*chi_r x (edges per channel) cMAC (counted)
+
+HBM bytes per evaluation (compulsory): theta (P reals) + gradient (P reals) + energy
+(16 B) + the stored right environments written once by RL and read once by LR.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def sweep_cmacs(plan) -> dict:
+    s = plan.sites
+    cl = s["chi_l"].astype(np.float64)
+    cr = s["chi_r"].astype(np.float64)
+    nops = s["op_count"].astype(np.float64)
+    pairs = cl * cr
+    fold = pairs * nops * 4
+    rl = 2 * s["rl_db"] * cl * cr * cr + 2 * s["rl_da"] * cl * cl * cr + 2 * s["rl_edge_count"] * cl * cr
+    lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl + 2 * s["lr_db"] * cl * cr * cr
+          + 2 * s["lr_edge_count"] * cl * cr)
+    adj = pairs * nops * 12
+    return {"rl": float(np.sum(fold + rl)), "lr": float(np.sum(fold + lr + adj)),
+            "fold": float(np.sum(fold)), "adjoint": float(np.sum(adj))}
+
+
+def env_bytes(plan, real_bytes: int = 4) -> float:
+    """Stored right-environment bytes for one theta-set (written once, read once)."""
+    return float(plan.env_total) * 2 * real_bytes
+
+
+def eval_model(plan, grad: bool = True, real_bytes: int = 4) -> dict:
+    """Per-evaluation (one theta-set) flops and compulsory HBM bytes."""
+    c = sweep_cmacs(plan)
+    flops_rl = 8 * c["rl"]
+    flops_lr = 8 * c["lr"] if grad else 0.0
+    P = plan.n_params
+    byts = P * real_bytes + 16
+    if grad:
+        byts += P * real_bytes + 2 * env_bytes(plan, real_bytes)
+    return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops": flops_rl + flops_lr, "bytes": byts,
+            "cmacs": c}

@@ -1,0 +1,29 @@
+"""Shared test helpers: golden documents -> product IR objects."""
+
+import numpy as np
+
+from paper_2112_10239_b200.circuits import Circuit, standard_gate
+from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, PauliTerm
+
+
+def to_circuit(doc):
+    gates = tuple(standard_gate(name, tuple(wires), param) for name, wires, param in doc["gates"])
+    return Circuit(doc["n"], gates, tuple(doc["trainable"]))
+
+
+def to_ham(doc, n):
+    return PauliHamiltonian(n, tuple(PauliTerm(complex(re, im), tuple((int(q), l) for q, l in ops))
+                                     for re, im, ops in doc))
+
+
+def tol64(ref_val, ham):
+    """complex64 energy tolerance: 1e-5 * max(|E|, 1e-2 * sum|c|)."""
+    s = sum(abs(t.coeff) for t in ham.terms)
+    return 1e-5 * max(abs(ref_val), 1e-2 * s, 1e-3)
+
+
+def grad_ok64(g, ref):
+    """|dg| <= 1e-5 |g_ref| + 1e-6 ||g_ref||_inf, with a 2e-6 floor for tiny vectors."""
+    ref = np.asarray(ref)
+    scale = max(np.max(np.abs(ref), initial=0.0), 1.0)
+    return np.all(np.abs(g - ref) <= 1e-5 * np.abs(ref) + 2e-6 * scale)

@@ -1,0 +1,159 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  complex64 at the SURVEY.md section 8c tolerances
+(relative 1e-5), complex128 at 1e-10."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected only on GPU runs
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+from conftest import ocircuit, oterms  # noqa: E402
+from helpers_engine import grad_ok64, to_circuit, to_ham, tol64  # noqa: E402
+from paper_2112_10239_b200 import autodiff as AD  # noqa: E402
+from paper_2112_10239_b200 import chain as C  # noqa: E402
+from paper_2112_10239_b200.circuits import Circuit, standard_gate  # noqa: E402
+from paper_2112_10239_b200.errors import BondTooLarge, InputError, ParamCountMismatch  # noqa: E402
+from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, term, tfim  # noqa: E402
+from paper_2112_10239_b200.workloads import CONFIGS, layered_circuit, theta_sets  # noqa: E402
+
+
+def _cases(golden_small):
+    for case in golden_small["cases"]:
+        c = to_circuit(case["circuit"])
+        h = to_ham(case["ham"], c.n_qubits)
+        yield case, c, h
+
+
+def test_golden_complex64(golden_small):
+    ran = 0
+    for case, c, h in _cases(golden_small):
+        try:
+            v, g = AD.grad_expval(c, h, case["theta"], dtype="complex64")
+        except BondTooLarge:
+            continue
+        ran += 1
+        assert abs(v - case["value"]) <= tol64(case["value"], h), (case["name"], v, case["value"])
+        assert grad_ok64(g, case["grad"]), (case["name"], np.max(np.abs(g - np.array(case["grad"]))))
+    assert ran >= 15
+
+
+def test_golden_complex128(golden_small):
+    ran = 0
+    for case, c, h in _cases(golden_small):
+        try:
+            v, g = AD.grad_expval(c, h, case["theta"], dtype="complex128")
+        except BondTooLarge:
+            continue
+        ran += 1
+        assert abs(v - case["value"]) < 1e-10 * max(1.0, abs(case["value"])), case["name"]
+        np.testing.assert_allclose(g, case["grad"], rtol=1e-10, atol=1e-11, err_msg=case["name"])
+    assert ran >= 12
+
+
+def test_segmentation_invariance():
+    c = layered_circuit(100, 10, "ry", "cz")
+    h = tfim(100)
+    th = theta_sets(c.n_params, 3, seed=5)
+    ref = [AD.grad_expval(c, h, th, dtype="complex128", segments=s) for s in (1, 4, 13)]
+    for v, g in ref[1:]:
+        np.testing.assert_allclose(v, ref[0][0], atol=1e-11)
+        np.testing.assert_allclose(g, ref[0][1], atol=1e-11)
+
+
+def test_cfg2_batch256_against_oracle(golden_small):
+    cfg = CONFIGS["cfg2"]
+    c, h = cfg.circuit(), cfg.hamiltonian()
+    th = theta_sets(c.n_params, 256, seed=0)
+    v, g = AD.grad_expval(c, h, th)
+    assert v.shape == (256,) and g.shape == (256, 500)
+    # b = 0..3 are the reference's golden vectors (make_golden.py)
+    for b in range(4):
+        case = golden_small["cases"][1 + b]
+        np.testing.assert_array_equal(th[b], np.array(case["theta"]))
+        assert abs(v[b] - case["value"]) <= tol64(case["value"], h)
+        assert grad_ok64(g[b], case["grad"])
+    # a few more sets against the oracle restatement
+    oc, ot = O.ry_cz_layers(100, 10), O.tfim_terms(100)
+    for b in (17, 255):
+        ov, og = O.grad_expval_tt(oc, ot, th[b])
+        assert abs(v[b] - ov) <= tol64(ov, h)
+        assert grad_ok64(g[b], og)
+
+
+def test_deterministic_repeats():
+    cfg = CONFIGS["cfg2"]
+    c, h = cfg.circuit(), cfg.hamiltonian()
+    th = theta_sets(c.n_params, 32, seed=1)
+    a = AD.grad_expval(c, h, th)
+    b = AD.grad_expval(c, h, th)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_closed_forms():
+    for t in (-1.3, 0.4, 2.9):
+        c = Circuit(1, (standard_gate("rx", (0,), t),), (0,))
+        v, g = AD.grad_expval(c, PauliHamiltonian(1, (term(1.0, {0: "Z"}),)), [t], dtype="complex128")
+        assert abs(v - np.cos(t)) < 1e-12 and abs(g[0] + np.sin(t)) < 1e-12
+    for n in (2, 5, 9):
+        v, _ = AD.grad_expval(Circuit(n, (), ()), tfim(n), [], dtype="complex128")
+        assert abs(v + (n - 1)) < 1e-12
+    c = Circuit(2, (standard_gate("h", (0,)), standard_gate("h", (1,)), standard_gate("crz", (0, 1), 0.9)), (2,))
+    ham = PauliHamiltonian(2, (term(1.0, {0: "X"}),))
+    v, g = AD.grad_expval(c, ham, [0.9], dtype="complex128")
+    assert abs(v - np.cos(0.45)) < 1e-12 and abs(g[0] + 0.5 * np.sin(0.45)) < 1e-12
+    shift = AD.parameter_shift_grad(c, ham, [0.9], dtype="complex128")
+    assert abs(shift[0] - g[0]) < 1e-12
+
+
+def test_product_chain_30_qubits():
+    # reference test_hamiltonians.py:96-107: ry product state, <Z_k> = cos t_k
+    rng = np.random.default_rng(3)
+    th = rng.uniform(-np.pi, np.pi, 30)
+    c = Circuit(30, tuple(standard_gate("ry", (q,), 0.0) for q in range(30)), tuple(range(30)))
+    ham = PauliHamiltonian(30, tuple(term(1.0, {q: "Z"}) for q in range(30)))
+    v = AD.evaluate_expval(c, ham, th, dtype="complex128")
+    assert abs(v - np.cos(th).sum()) < 1e-12
+    vals = AD.expectation_values(c, th, [{3: "Z", 17: "Z"}, {5: "X"}], dtype="complex128")
+    assert abs(vals[0] - np.cos(th[3]) * np.cos(th[17])) < 1e-12
+    assert abs(vals[1] - np.sin(th[5])) < 1e-12
+
+
+def test_values_match_oracle(golden_small):
+    case = golden_small["cases"][0]
+    c = to_circuit(case["circuit"])
+    groups = [{0: "Z"}, {3: "X", 4: "Y"}, {2: "Z", 7: "X"}, {}, {9: "Y"}]
+    vals = AD.expectation_values(c, case["theta"], groups, dtype="complex128")
+    ref = O.taped_term_values(ocircuit(case["circuit"]), np.array(case["theta"]),
+                              [tuple(sorted(g.items())) for g in groups])
+    np.testing.assert_allclose(vals, ref, atol=1e-12)
+
+
+def test_cfg4_energy_and_shift_coordinates(golden_large):
+    cfg = CONFIGS["cfg4"]
+    c, h = cfg.circuit(), cfg.hamiltonian()
+    th = golden_large["cfg4_theta"]
+    v, g = AD.grad_expval(c, h, th)
+    e_ref = float(golden_large["cfg4_E"])
+    assert abs(v - e_ref) <= tol64(e_ref, h), (v, e_ref)
+    gnorm = max(np.max(np.abs(g)), 1.0)
+    for k, ref in zip(golden_large["cfg4_coords"], golden_large["cfg4_shift"]):
+        assert abs(g[k] - ref) <= 1e-5 * abs(ref) + 2e-6 * gnorm, (k, g[k], ref)
+
+
+def test_error_taxonomy():
+    c = layered_circuit(4, 2)
+    with pytest.raises(ParamCountMismatch):
+        AD.grad_expval(c, tfim(4), np.zeros(3))
+    with pytest.raises(InputError):
+        AD.grad_expval(c, tfim(4), np.full(4, np.nan))
+    with pytest.raises(InputError):
+        AD.grad_expval(c, tfim(4), np.zeros(4), engine="dense")
+    wide = Circuit(8, tuple(standard_gate("cnot", (0, 7)) for _ in range(6)), ())
+    with pytest.raises(BondTooLarge):
+        AD.evaluate_expval(wide, tfim(8), [])

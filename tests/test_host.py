@@ -1,0 +1,114 @@
+"""CPU-only tests: chain compiler + numpy kernel mirror against the oracle, the
+C-ABI library's exports and struct layouts (no compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import mirror
+import oracle as O
+from helpers_engine import to_circuit, to_ham
+from paper_2112_10239_b200 import chain as C
+from paper_2112_10239_b200.circuits import Circuit, standard_gate
+from paper_2112_10239_b200.errors import BondTooLarge
+from paper_2112_10239_b200.hamiltonians import tfim
+from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_mirror_matches_reference_golden(golden_small):
+    ran = 0
+    for case in golden_small["cases"]:
+        c = to_circuit(case["circuit"])
+        if c.n_qubits > 12:
+            continue
+        h = to_ham(case["ham"], c.n_qubits)
+        terms = C.normalize_terms(h)
+        for segs in (1, 3):
+            try:
+                plan = C.compile_chain(c, terms, "energy", segments=segs)
+            except BondTooLarge:
+                continue
+            coef = np.array([t[0].real for t in terms])
+            e, g = mirror.energy_grad(plan, np.array(case["theta"]), coef)
+            assert abs(e.real - case["value"]) < 1e-12, case["name"]
+            np.testing.assert_allclose(g, case["grad"], atol=1e-12)
+            ran += 1
+    assert ran >= 20
+
+
+def test_mirror_values_and_segments_cfg2(golden_small):
+    case = golden_small["cases"][1]
+    c = to_circuit(case["circuit"])
+    h = to_ham(case["ham"], c.n_qubits)
+    terms = C.normalize_terms(h)
+    plan = C.compile_chain(c, terms, "values", segments=4)
+    vals = mirror.term_values(plan, np.array(case["theta"]))
+    e = sum(t[0] * v for t, v in zip(terms, vals))
+    assert abs(e.real - case["value"]) < 1e-12
+
+
+def test_factored_bond_dimensions_match_survey():
+    # SURVEY.md section 8 shorthand: chi per config under reading A
+    for n, layers, ent, chi in ((10, 4, "cnot", 2), (100, 10, "cz", 8), (1000, 20, "cz", 32), (64, 10, "cz", 8)):
+        c = layered_circuit(n, layers, "ry", ent)
+        plan = C.compile_chain(c, C.normalize_terms(tfim(n)), "energy", segments=1)
+        assert plan.chi_max == chi, (n, layers, plan.chi_max)
+
+
+def test_light_cone_segments_cover_terms():
+    c = layered_circuit(100, 10)
+    terms = C.normalize_terms(tfim(100))
+    plan = C.compile_chain(c, terms, "energy", segments=8)
+    assert plan.n_segments == 8
+    lo, hi = plan.segs["lo"], plan.segs["hi"]
+    assert lo[0] == 0 and hi[-1] == 99
+    # every trainable slot is covered by at least one segment
+    assert np.all(np.diff(plan.gred_ptr) >= 1)
+
+
+def test_operator_schmidt_split():
+    for name in ("cz", "cnot", "swap"):
+        g = standard_gate(name, (0, 1))
+        bits, f0, f1 = C.split_two_qubit(g.matrix)
+        rebuilt = sum(np.kron(a, b) for a, b in zip(f0, f1))
+        np.testing.assert_allclose(rebuilt, g.matrix, atol=1e-14)
+        assert bits == (2 if name == "swap" else 1)
+
+
+def test_bond_limit_raises():
+    wide = Circuit(8, tuple(standard_gate("cnot", (0, 7)) for _ in range(6)), ())
+    with pytest.raises(BondTooLarge):
+        C.compile_chain(wide, C.normalize_terms(tfim(8)), "energy")
+
+
+def _lib_path():
+    return os.path.join(ROOT, "paper_2112_10239_b200", "libtq_engine.so")
+
+
+def test_library_exports_every_header_symbol():
+    path = _lib_path()
+    if not os.path.exists(path):
+        pytest.skip("library not built")
+    import torch  # noqa: F401  (provides libcudart.so.12 to the loader)
+    from paper_2112_10239_b200 import _lib
+
+    header = open(os.path.join(ROOT, "include", "tq_engine.h")).read()
+    declared = set(re.findall(r"\b(tq_[a-z_]+)\s*\(", header))
+    assert declared == set(_lib.EXPORTED_SYMBOLS)
+    lib = ctypes.CDLL(path)
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert _lib.abi_sizes() == _lib.NUMPY_SIZES
+    assert b"sm_100a" in _lib.load().tq_build_info()
+
+
+def test_theta_sets_are_float32_exact():
+    th = theta_sets(500, 4, seed=0)
+    np.testing.assert_array_equal(th, th.astype(np.float32).astype(np.float64))
+    g = np.array(O.generator(0).uniform(-np.pi, np.pi, 500))
+    np.testing.assert_array_equal(theta_sets(500, 1, seed=0)[0], g.astype(np.float32).astype(np.float64))
