@@ -58,7 +58,7 @@ typedef struct {
   int32_t rl_edge_begin, rl_edge_count, lr_edge_begin, lr_edge_count;
   int32_t fin_begin, fin_count;
   int32_t rl_da, rl_db, lr_da, lr_db;
-  int32_t n_train, pad0;
+  int32_t n_train, ent_begin; /* ent_begin: first of this site's contiguous tq_mat entries */
   int64_t env_in, env_out;  /* complex offsets of the stored right envs at cut k+1 / cut k (-1: none) */
   double init[4];           /* input product-state vector of this qubit (re,im,re,im) */
 } tq_site;
@@ -94,6 +94,7 @@ typedef struct {
 typedef struct {
   int32_t n_segments, n_sites, n_params, n_terms;
   int32_t chi_max, d_max, max_ops, max_lmat, max_train, n_gslots;
+  int32_t max_edges, pad0;
   int64_t env_total; /* complex elements of stored envs per theta-set */
   double e_const_re, e_const_im; /* identity-term coefficients */
   const tq_site* sites;

@@ -284,3 +284,34 @@ def minimize(fun, theta0, optimizer: str = "gd", rate: float = 0.05, max_iters: 
             vhat = v / (1 - b2 ** (it + 1))
             theta = theta - rate * mhat / (np.sqrt(vhat) + adam_eps)
     return MinimizeResult(tuple(steps), False)
+
+
+def state_inner_product(ket_circuit: Circuit, ket_theta, bra_circuit: Circuit | None = None, bra_theta=None, *,
+                        ket_init=None, bra_init=None, dtype: str = "complex64", device=None):
+    """<bra|ket> with |ket> = U_ket(theta)|ket_init>, |bra> = U_bra(theta')|bra_init>
+    (the first argument of the reference's tt_inner is conjugated, tt.py:247-255).
+
+    ``bra_circuit=None`` means no gates on the bra side (a product state, e.g. tlquantum's
+    ``state_inner_product(state, compare_state)`` = <compare|U|state>).  Init vectors are
+    per-qubit complex 2-vectors (default |0>).  theta may be batched [B, P]."""
+    n = ket_circuit.n_qubits
+    bra_circuit = bra_circuit if bra_circuit is not None else Circuit(n, (), ())
+    if bra_circuit.n_qubits != n:
+        from .errors import SizeMismatch
+        raise SizeMismatch(f"{bra_circuit.n_qubits} vs {n} qubits")
+    tk, single = _check_theta(ket_circuit, ket_theta)
+    tb, _ = _check_theta(bra_circuit, np.zeros((tk.shape[0], 0)) if bra_theta is None else bra_theta)
+    if tb.shape[0] == 1 and tk.shape[0] > 1:
+        tb = np.repeat(tb, tk.shape[0], axis=0)
+    dev = _device(device)
+    limit = C.MAX_CHI if dtype == "complex64" else C.MAX_CHI_F64
+
+    def plan(circ, init):
+        key_terms = []
+        return E.device_plan(circ, key_terms, "state", 1, dev, 1, init=init, dtype=dtype)
+
+    dk, db = plan(ket_circuit, ket_init), plan(bra_circuit, bra_init)
+    tdt = E.DTYPES[dtype][1]
+    out = E.inner_raw(db, torch.tensor(tb, dtype=tdt, device=dev), dk, torch.tensor(tk, dtype=tdt, device=dev),
+                      dtype).cpu().numpy()
+    return complex(out[0]) if single else out

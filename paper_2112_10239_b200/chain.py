@@ -43,7 +43,7 @@ SITE_DTYPE = np.dtype([
     ("rl_edge_begin", "<i4"), ("rl_edge_count", "<i4"), ("lr_edge_begin", "<i4"), ("lr_edge_count", "<i4"),
     ("fin_begin", "<i4"), ("fin_count", "<i4"),
     ("rl_da", "<i4"), ("rl_db", "<i4"), ("lr_da", "<i4"), ("lr_db", "<i4"),
-    ("n_train", "<i4"), ("pad0", "<i4"),
+    ("n_train", "<i4"), ("ent_begin", "<i4"),
     ("env_in", "<i8"), ("env_out", "<i8"),
     ("init", "<f8", (4,)),
 ], align=True)
@@ -219,20 +219,53 @@ def _cones_vectorized(tgates, los, his):
     return los, his
 
 
+def factored_chi(n, tgates) -> int:
+    """Largest factored bond 2^(bits crossing a cut) of the whole chain."""
+    bits = np.zeros(n + 1, dtype=np.int64)
+    for g in tgates:
+        if g.bits:
+            bits[g.lo + 1: g.hi + 1] += g.bits
+    return int(1 << int(bits.max())) if n else 1
+
+
+def resident_teams(chi: int, d: int = 3) -> int:
+    """Work items resident per SM, from the kernels' shared-memory layout (lr sweep,
+    complex64): (4 + 6D) matrix slots of (chi+1)^2 complex plus descriptors.  Warp
+    teams (chi <= 8) come 4 per CTA; chi 16/32 teams are whole CTAs."""
+    b = 2
+    while b < chi:
+        b <<= 1
+    team_bytes = (4 + 6 * d) * (b + 1) ** 2 * 8 + 4096
+    smem = 227 * 1024
+    if b <= 8:
+        ctas = max(1, smem // (4 * team_bytes))
+        return int(min(ctas * 4, 64))
+    return int(max(1, min(smem // team_bytes, 2048 // (128 if b == 16 else 256))))
+
+
 def choose_segments(n, terms, tgates, batch, n_sm=148, requested=None):
-    """How many segments per theta-set.  Enough CTAs to fill the chip while the
-    light-cone halo keeps redundancy below ~2x."""
+    """Segments per theta-set.  Minimises waves x sites-per-item, where a segment
+    costs its owned sites plus the light-cone halo, and a wave is one resident item
+    per team slot on every SM."""
     if requested is not None:
         return max(1, int(requested))
     firsts = sorted({ops[0][0] for _, ops in terms if ops})
     if not firsts:
         return 1
     mid = firsts[len(firsts) // 2]
-    clo, chi = light_cone(tgates, mid, mid + 1 if mid + 1 < n else mid)
-    width = max(1, chi - clo + 1)
-    want = max(1, math.ceil(4 * n_sm / max(1, batch)))
-    cap = max(1, len(firsts) // max(1, width))
-    return int(max(1, min(want, cap, 512)))
+    clo, chi_ = light_cone(tgates, mid, mid + 1 if mid + 1 < n else mid)
+    width = max(1, chi_ - clo + 1)
+    chi = factored_chi(n, tgates)
+    res = resident_teams(min(chi, 32))
+    slots = n_sm * res
+    nf = len(firsts)
+    best, best_cost = 1, None
+    for S in range(1, min(nf, 1024) + 1):
+        waves = math.ceil(batch * S / slots)
+        cost = waves * (nf / S + width)
+        if best_cost is None or cost < best_cost - 1e-9:
+            best, best_cost = S, cost
+    return best
 
 
 # ----------------------------------------------------------------------------- plan
@@ -253,6 +286,7 @@ class ChainPlan:
     gred_idx: np.ndarray
     chi_max: int
     d_max: int
+    max_edges: int
     max_ops: int
     max_lmat: int
     max_train: int
@@ -290,21 +324,24 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         for q, _ in ops:
             if not 0 <= q < n:
                 raise WireOutOfRange(f"term acts on qubit {q} but n_qubits={n}")
-    S = choose_segments(n, ham_terms, tg, batch, n_sm, segments)
-    firsts = sorted({ops[0][0] for _, ops in ham_terms if ops})
-    ranges = _segment_ranges(firsts, min(S, max(1, len(firsts)))) if firsts else []
-    # owned terms per range
-    owned = [[] for _ in ranges]
-    starts = [r[0] for r in ranges]
-    for t, (_, ops) in enumerate(ham_terms):
-        if not ops:
-            continue
-        f = ops[0][0]
-        gi = int(np.searchsorted(starts, f, side="right") - 1)
-        owned[gi].append(t)
-    los = [min(ham_terms[t][1][0][0] for t in ow) for ow in owned]
-    his = [max(ham_terms[t][1][-1][0] for t in ow) for ow in owned]
-    clos, chis = _cones_vectorized(tg, los, his)
+    if mode == "state":   # the whole chain, no operator (inner products)
+        owned, clos, chis = [[]], np.array([0]), np.array([n - 1])
+    else:
+        S = choose_segments(n, ham_terms, tg, batch, n_sm, segments)
+        firsts = sorted({ops[0][0] for _, ops in ham_terms if ops})
+        ranges = _segment_ranges(firsts, min(S, max(1, len(firsts)))) if firsts else []
+        # owned terms per range
+        owned = [[] for _ in ranges]
+        starts = [r[0] for r in ranges]
+        for t, (_, ops) in enumerate(ham_terms):
+            if not ops:
+                continue
+            f = ops[0][0]
+            gi = int(np.searchsorted(starts, f, side="right") - 1)
+            owned[gi].append(t)
+        los = [min(ham_terms[t][1][0][0] for t in ow) for ow in owned]
+        his = [max(ham_terms[t][1][-1][0] for t in ow) for ow in owned]
+        clos, chis = _cones_vectorized(tg, los, his)
 
     sites, ops, mats, edges, fins, passes, segs = [], [], [], [], [], [], []
     mat_index = {}
@@ -327,15 +364,14 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         return rec
 
     def mat_block(specs):
-        """Contiguous table entries for one op (entry = base + digit); singletons deduplicated."""
-        if len(specs) == 1:
-            key = (specs[0].kind, specs[0].slot, specs[0].const)
-            if key not in mat_index:
-                mat_index[key] = len(mats)
-                mats.append(make_rec(specs[0]))
-            return mat_index[key]
+        """Table entries for one op (entry = base + digit), appended in op order so every
+        site's entries are contiguous (the kernel resolves entry e of a site at ent_begin + e)."""
         base = len(mats)
-        mats.extend(make_rec(s) for s in specs)
+        for spec in specs:
+            key = (spec.kind, spec.slot, spec.const)
+            if key not in mat_index:
+                mat_index[key] = make_rec(spec)
+            mats.append(mat_index[key])
         return base
 
     for gi_seg, (ow, c_lo, c_hi) in enumerate(zip(owned, clos.tolist(), chis.tolist())):
@@ -367,7 +403,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         # ---- MPO channels
         ow_terms = [(t, ham_terms[t][1]) for t in ow]
         rl_ch, lr_ch, rl_edges, lr_edges, fin_list = _build_mpo(ow_terms, c_lo, nsite, mode)
-        d_max = max(d_max, max(len(x) for x in rl_ch), max(len(x) for x in lr_ch))
+        d_max = max(d_max, max(len(x) for x in rl_ch), max(len(x) for x in lr_ch), 1)
 
         # ---- env offsets (RL channel envs stored at cuts 1..nsite)
         env_off = np.full(nsite + 1, -1, dtype=np.int64)
@@ -384,6 +420,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         for q in range(nsite):
             rec = np.zeros((), dtype=SITE_DTYPE)
             rec["op_begin"] = len(ops)
+            rec["ent_begin"] = len(mats)
             lmat = 0
             ntrain = 0
             for (src, shift, bits, specs) in col[q]:
@@ -456,12 +493,19 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         sites=arr(sites, SITE_DTYPE), ops=arr(ops, OP_DTYPE), mats=arr(mats, MAT_DTYPE),
         edges=arr(edges, EDGE_DTYPE), fins=arr(fins, EDGE_DTYPE), passes=arr(passes, PASS_DTYPE),
         segs=arr(segs, SEG_DTYPE), gred_ptr=ptr, gred_idx=np.array(idx, dtype=np.int32),
-        chi_max=chi_max, d_max=d_max, max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
+        chi_max=chi_max, d_max=d_max, max_edges=_max_edges(sites), max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
         n_gslots=gslot_total, env_total=env_total, e_const=e_const, term_active=active,
     )
     plan.info = {"segments": len(segs), "sub_chain_sites": int(sum(int(s["site_count"]) for s in segs)),
                  "chi_max": chi_max, "d_max": d_max}
     return plan
+
+
+def _max_edges(sites):
+    m = 1
+    for r in sites:
+        m = max(m, int(r["rl_edge_count"]), int(r["lr_edge_count"]), int(r["fin_count"]))
+    return m
 
 
 def _edge(a, b, op, coef):
@@ -522,6 +566,9 @@ def _build_mpo(ow_terms, c_lo, nsite, mode):
             rl_edges[k] = el
             lr_edges[k] = el
         return ch, ch, rl_edges, lr_edges, fins
+    if mode == "state":
+        empty = [{} for _ in range(nsite + 1)]
+        return empty, empty, rl_edges, lr_edges, fins
     if mode != "values":
         raise InputError(f"unknown plan mode {mode!r}")
     rl_ch = [{"D": 0} for _ in range(nsite + 1)]

@@ -49,10 +49,20 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
 
 // ------------------------------------------------------------------ kernel parameters
 struct Layout {          // byte offsets inside one team's shared-memory slab (host computed)
-  int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps;
+  int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, sedge;
   int32_t team_bytes;
-  int32_t nslot_env, nslot_m, nslot_br, nslot_pin, nslot_mr;
 };
+
+// Site edge staged in shared memory with its coefficient already resolved for this theta-set.
+template <typename R> struct SEdge { int a, b, op; R coef; };
+
+// Packed column op: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24]
+__device__ __forceinline__ int oc_lmat(int c) { return c & 511; }
+__device__ __forceinline__ int oc_tidx(int c) { return ((c >> 18) & 63) - 1; }
+__device__ __forceinline__ int oc_digit(int c, int al, int be) {
+  const int src = (c >> 9) & 3, shift = (c >> 11) & 31, mask = (1 << ((c >> 16) & 3)) - 1;
+  return src == 0 ? 0 : (((src == 1 ? al : be) >> shift) & mask);
+}
 
 struct Params {
   tq_chain c;
@@ -73,14 +83,6 @@ template <int TEAM> __device__ __forceinline__ void team_sync() {
   if (TEAM == 32) __syncwarp(); else __syncthreads();
 }
 
-template <typename R> __device__ __forceinline__ R theta_at(const Params& p, int b, int slot) {
-  return reinterpret_cast<const R*>(p.theta)[(int64_t)b * p.theta_stride + slot];
-}
-template <typename R> __device__ __forceinline__ R coef_at(const Params& p, int b, int idx) {
-  if (idx < 0) return R(1);
-  return reinterpret_cast<const R*>(p.coef)[(int64_t)b * p.coef_stride + idx];
-}
-
 // Pauli op element <s'|O|s>: for op in {I,X,Y,Z} the only nonzero s for a given s' and its factor.
 template <typename C> __device__ __forceinline__ int pauli_src(int op, int sp) { return (op == 1 || op == 2) ? 1 - sp : sp; }
 template <typename C> __device__ __forceinline__ C pauli_fac(int op, int sp) {
@@ -91,47 +93,51 @@ template <typename C> __device__ __forceinline__ C pauli_fac(int op, int sp) {
 }
 
 // ------------------------------------------------------------------ stage helpers
-// Resolve the site's 2x2 factor table for this theta-set into shared memory.
+// Stage one site's descriptors for this theta-set into shared memory: the resolved
+// 2x2 factors (entry e of the site lives at mats[ent_begin + e]), packed op codes and
+// the MPO edges of the current sweep with their coefficients looked up once.
 template <typename R, int TEAM>
-__device__ void resolve_mats(const Params& p, const tq_site& st, int b, int tid,
-                             typename CT<R>::T* mres, int* minfo, R* mps) {
+__device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef_row, const tq_site& st, int tid, bool rl,
+                           typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, SEdge<R>* sedge) {
   using C = typename CT<R>::T;
-  for (int oi = 0; oi < st.op_count; ++oi) {
-    const tq_op op = p.c.ops[st.op_begin + oi];
-    const int nd = 1 << op.bits;
-    for (int d = 0; d < nd; ++d) {
-      const int e = op.lmat + d;
-      if ((e % TEAM) != tid) continue;
-      const tq_mat mt = p.c.mats[op.mat + d];
-      C m00, m01, m10, m11;
-      if (mt.kind == 0) {
-        m00 = cmk<C>(R(mt.m[0]), R(mt.m[1])); m01 = cmk<C>(R(mt.m[2]), R(mt.m[3]));
-        m10 = cmk<C>(R(mt.m[4]), R(mt.m[5])); m11 = cmk<C>(R(mt.m[6]), R(mt.m[7]));
-      } else {
-        const R t = mt.slot >= 0 ? theta_at<R>(p, b, mt.slot) : R(mt.angle);
-        R s, c;
-        if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); s = R(sf); c = R(cf); }
-        else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); s = R(sd); c = R(cd); }
-        const R z = R(0);
-        if (mt.kind == 1) { m00 = cmk<C>(c, z); m01 = cmk<C>(z, -s); m10 = cmk<C>(z, -s); m11 = cmk<C>(c, z); }
-        else if (mt.kind == 2) { m00 = cmk<C>(c, z); m01 = cmk<C>(-s, z); m10 = cmk<C>(s, z); m11 = cmk<C>(c, z); }
-        else { m00 = cmk<C>(c, -s); m01 = cmk<C>(z, z); m10 = cmk<C>(z, z); m11 = cmk<C>(c, s); }
-      }
-      mres[4 * e + 0] = m00; mres[4 * e + 1] = m01; mres[4 * e + 2] = m10; mres[4 * e + 3] = m11;
-      minfo[e] = (mt.kind & 0xff) | ((mt.cls & 0xff) << 8);
-      mps[e] = R(mt.pscale);
+  for (int e = tid; e < st.lmat_count; e += TEAM) {
+    const tq_mat& mt = ch.mats[st.ent_begin + e];
+    const int kind = mt.kind;
+    C m00, m01, m10, m11;
+    if (kind == 0) {
+      m00 = cmk<C>(R(mt.m[0]), R(mt.m[1])); m01 = cmk<C>(R(mt.m[2]), R(mt.m[3]));
+      m10 = cmk<C>(R(mt.m[4]), R(mt.m[5])); m11 = cmk<C>(R(mt.m[6]), R(mt.m[7]));
+    } else {
+      const R t = mt.slot >= 0 ? theta_row[mt.slot] : R(mt.angle);
+      R sn, cs;
+      if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); sn = R(sf); cs = R(cf); }
+      else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); sn = R(sd); cs = R(cd); }
+      const R z = R(0);
+      if (kind == 1) { m00 = cmk<C>(cs, z); m01 = cmk<C>(z, -sn); m10 = cmk<C>(z, -sn); m11 = cmk<C>(cs, z); }
+      else if (kind == 2) { m00 = cmk<C>(cs, z); m01 = cmk<C>(-sn, z); m10 = cmk<C>(sn, z); m11 = cmk<C>(cs, z); }
+      else { m00 = cmk<C>(cs, -sn); m01 = cmk<C>(z, z); m10 = cmk<C>(z, z); m11 = cmk<C>(cs, sn); }
     }
+    mres[4 * e + 0] = m00; mres[4 * e + 1] = m01; mres[4 * e + 2] = m10; mres[4 * e + 3] = m11;
+    minfo[e] = (kind & 0xff) | ((mt.cls & 0xff) << 8);
+    mps[e] = R(1) / R(mt.pscale);   // reciprocal: the adjoint rebuilds v[a] = v'[a] / pscale
+  }
+  for (int o = tid; o < st.op_count; o += TEAM) {
+    const tq_op& op = ch.ops[st.op_begin + o];
+    ocode[o] = op.lmat | (op.src << 9) | (op.shift << 11) | (op.bits << 16) | ((op.tidx + 1) << 18);
+    ogidx[o] = op.gidx;
+  }
+  const int eb = rl ? st.rl_edge_begin : st.lr_edge_begin;
+  const int ec = rl ? st.rl_edge_count : st.lr_edge_count;
+  for (int ei = tid; ei < ec; ei += TEAM) {
+    const tq_edge ed = ch.edges[eb + ei];
+    SEdge<R> se; se.a = ed.a; se.b = ed.b; se.op = ed.op; se.coef = ed.coef < 0 ? R(1) : coef_row[ed.coef];
+    sedge[ei] = se;
   }
 }
 
-__device__ __forceinline__ int op_digit(const tq_op& op, int al, int be) {
-  const int mask = (1 << op.bits) - 1;
-  return op.src == 1 ? ((al >> op.shift) & mask) : (op.src == 2 ? ((be >> op.shift) & mask) : 0);
-}
-
-__device__ __forceinline__ bool pass_ok(const Params& p, const tq_site& st, int al, int be) {
+__device__ __forceinline__ bool pass_ok(const tq_chain& ch, const tq_site& st, int al, int be) {
   for (int i = 0; i < st.pass_count; ++i) {
-    const tq_pass ps = p.c.passes[st.pass_begin + i];
+    const tq_pass ps = ch.passes[st.pass_begin + i];
     const int m = (1 << ps.bits) - 1;
     if (((al >> ps.sa) & m) != ((be >> ps.sb) & m)) return false;
   }
@@ -140,19 +146,19 @@ __device__ __forceinline__ bool pass_ok(const Params& p, const tq_site& st, int 
 
 // Fold the column of site st into A[s] (chi_l x chi_r, row stride LD) and AH[s] = A[s]^H.
 template <typename R, int LD, int TEAM>
-__device__ void fold_site(const Params& p, const tq_site& st, int tid, const typename CT<R>::T* mres,
-                          typename CT<R>::T* A, typename CT<R>::T* AH, int lcr) {
+__device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                          const int* ocode, typename CT<R>::T* A, typename CT<R>::T* AH, int lcr) {
   using C = typename CT<R>::T;
   const int npair = st.chi_l * st.chi_r;
   for (int pi = tid; pi < npair; pi += TEAM) {
     const int al = pi >> lcr, be = pi & (st.chi_r - 1);
     C v0 = cmk<C>(R(st.init[0]), R(st.init[1]));
     C v1 = cmk<C>(R(st.init[2]), R(st.init[3]));
-    if (!pass_ok(p, st, al, be)) { v0 = cmk<C>(R(0), R(0)); v1 = v0; }
+    if (st.pass_count && !pass_ok(ch, st, al, be)) { v0 = cmk<C>(R(0), R(0)); v1 = v0; }
     else {
       for (int oi = 0; oi < st.op_count; ++oi) {
-        const tq_op op = p.c.ops[st.op_begin + oi];
-        const C* M = mres + 4 * (op.lmat + op_digit(op, al, be));
+        const int c = ocode[oi];
+        const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al, be));
         C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
         C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
         v0 = n0; v1 = n1;
@@ -203,6 +209,63 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
   }
 }
 
+// ------------------------------------------------------------------ shared-memory carving
+template <typename R>
+struct TeamSmem {
+  using C = typename CT<R>::T;
+  C *A, *AH, *ENV, *M, *BR, *PIN, *MR, *mres;
+  R *contrib, *mps;
+  int *minfo, *ocode, *ogidx;
+  SEdge<R>* sedge;
+  __device__ TeamSmem(unsigned char* base, const Layout& L) {
+    A = reinterpret_cast<C*>(base + L.a); AH = reinterpret_cast<C*>(base + L.ah);
+    ENV = reinterpret_cast<C*>(base + L.env); M = reinterpret_cast<C*>(base + L.m);
+    BR = reinterpret_cast<C*>(base + L.br); PIN = reinterpret_cast<C*>(base + L.pin);
+    MR = reinterpret_cast<C*>(base + L.mr); mres = reinterpret_cast<C*>(base + L.mres);
+    contrib = reinterpret_cast<R*>(base + L.contrib); mps = reinterpret_cast<R*>(base + L.mps);
+    minfo = reinterpret_cast<int*>(base + L.minfo); ocode = reinterpret_cast<int*>(base + L.ocode);
+    ogidx = reinterpret_cast<int*>(base + L.ogidx); sedge = reinterpret_cast<SEdge<R>*>(base + L.sedge);
+  }
+};
+
+// BR[t][s'] = sum over staged edges with target t of coef * <s'|O|s> * SRC[src][s]
+// (elementwise over chi_l x chi_r; `rl` selects which edge end is the target).
+template <typename R, int LD, int TEAM>
+__device__ __forceinline__ void bracket_stage(int tid, int ntarget, int ec, const SEdge<R>* sedge, bool rl,
+                                              const typename CT<R>::T* SRC, typename CT<R>::T* BR,
+                                              int lcl, int lcr) {
+  using C = typename CT<R>::T;
+  constexpr int MS = LD * LD;
+  const int lpair = lcl + lcr;
+  const int nel = (ntarget * 2) << lpair;
+  for (int e = tid; e < nel; e += TEAM) {
+    const int ij = e & ((1 << lpair) - 1);
+    const int ts = e >> lpair;
+    const int t = ts >> 1, sp = ts & 1;
+    const int off = (ij >> lcr) * LD + (ij & ((1 << lcr) - 1));
+    R ax = R(0), ay = R(0);
+    for (int ei = 0; ei < ec; ++ei) {
+      const SEdge<R> ed = sedge[ei];
+      if ((rl ? ed.a : ed.b) != t) continue;
+      const int src = rl ? ed.b : ed.a;
+      const int s = pauli_src<C>(ed.op, sp);
+      const C f = pauli_fac<C>(ed.op, sp);
+      const C nv = SRC[(src * 2 + s) * MS + off];
+      const C tt = cmul(f, nv);
+      ax = fma(ed.coef, tt.x, ax);
+      ay = fma(ed.coef, tt.y, ay);
+    }
+    BR[ts * MS + off] = cmk<C>(ax, ay);
+  }
+}
+
+template <typename C, int LD>
+__device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3) {
+  o[0] = a0;
+  if (rt > 1) o[LD] = a1;
+  if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
+}
+
 // ------------------------------------------------------------------ right-to-left sweep
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
@@ -211,7 +274,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
-  constexpr int MS = LD * LD;   // complex elements per matrix slot
+  constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
@@ -220,77 +283,46 @@ rl_sweep(Params p) {
   const int S = p.c.n_segments;
   if (item >= p.batch * S) return;
   const int b = item / S, g = item % S;
-  unsigned char* base = smem_raw + (size_t)team * p.L.team_bytes;
-  C* A = reinterpret_cast<C*>(base + p.L.a);
-  C* AH = reinterpret_cast<C*>(base + p.L.ah);
-  C* PIN = reinterpret_cast<C*>(base + p.L.env);
-  C* N = reinterpret_cast<C*>(base + p.L.m);
-  C* BR = reinterpret_cast<C*>(base + p.L.br);
-  C* mres = reinterpret_cast<C*>(base + p.L.mres);
-  int* minfo = reinterpret_cast<int*>(base + p.L.minfo);
-  R* mps = reinterpret_cast<R*>(base + p.L.mps);
+  TeamSmem<R> sm(smem_raw + (size_t)team * p.L.team_bytes, p.L);
+  const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
+  const R* coef_b = p.coef ? reinterpret_cast<const R*>(p.coef) + (int64_t)b * p.coef_stride : nullptr;
+  C* PIN = sm.ENV;   // P at the right cut (in) / left cut (out)
+  C* N = sm.M;
 
   const tq_segment seg = p.c.segs[g];
   C* env_g = reinterpret_cast<C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
-  // boundary: DONE channel = [[1]] at the right end of the sub-chain
-  if (tid == 0) PIN[0] = cmk<C>(R(1), R(0));
-  team_sync<TEAM>();
-  {
+  if (tid == 0) {
+    PIN[0] = cmk<C>(R(1), R(0));   // DONE channel = [[1]] at the right end
     const tq_site last = p.c.sites[seg.site_begin + seg.site_count - 1];
-    if (p.store_env && tid == 0 && last.env_in >= 0) env_g[last.env_in] = PIN[0];
+    if (p.store_env && last.env_in >= 0) env_g[last.env_in] = PIN[0];
   }
   for (int q = seg.site_count - 1; q >= 0; --q) {
     const tq_site st = p.c.sites[seg.site_begin + q];
     const int cl = st.chi_l, cr = st.chi_r;
-    const int lcr = 31 - __clz(cr);
-    resolve_mats<R, TEAM>(p, st, b, tid, mres, minfo, mps);
+    const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
+    const int db = st.rl_db, da = st.rl_da;
+    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, true, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.sedge);
     team_sync<TEAM>();
-    fold_site<R, LD, TEAM>(p, st, tid, mres, A, AH, lcr);
+    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
     team_sync<TEAM>();
     // N[b][s] = A[s] * P[b]
-    const int db = st.rl_db, da = st.rl_da;
     gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-        [&](int t, int) { return A + (t & 1) * MS; },
+        [&](int t, int) { return sm.A + (t & 1) * MS; },
         [&](int t, int) { return PIN + (t >> 1) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-          C* o = N + t * MS + i0 * LD + j;
-          o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
-        });
+        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     team_sync<TEAM>();
-    // BR[a][s'] = sum over edges (a <- bb) of coef * O_{s's} N[bb][s]
-    {
-      const int nel = da * 2 * cl * cr;
-      for (int e = tid; e < nel; e += TEAM) {
-        const int ij = e % (cl * cr);
-        const int as = e / (cl * cr);
-        const int a = as >> 1, sp = as & 1;
-        const int i = ij >> lcr, j = ij & (cr - 1);
-        C acc = cmk<C>(R(0), R(0));
-        for (int ei = 0; ei < st.rl_edge_count; ++ei) {
-          const tq_edge ed = p.c.edges[st.rl_edge_begin + ei];
-          if (ed.a != a) continue;
-          const R cf = coef_at<R>(p, b, ed.coef);
-          const int s = pauli_src<C>(ed.op, sp);
-          const C f = pauli_fac<C>(ed.op, sp);
-          const C nv = N[(ed.b * 2 + s) * MS + i * LD + j];
-          const C t = cmul(f, nv);
-          acc.x += cf * t.x; acc.y += cf * t.y;
-        }
-        BR[(a * 2 + sp) * MS + i * LD + j] = acc;
-      }
-    }
+    bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
     team_sync<TEAM>();
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     const bool store = p.store_env && st.env_out >= 0;
     C* envo = env_g + (store ? st.env_out : 0);
     gemm_group<C, LD, TEAM>(tid, da, cl, cl, cr, 2,
-        [&](int t, int qq) { return BR + (t * 2 + qq) * MS; },
-        [&](int, int qq) { return AH + qq * MS; },
+        [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
+        [&](int, int qq) { return sm.AH + qq * MS; },
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-          C* o = PIN + t * MS + i0 * LD + j;
-          o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
+          store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
           if (store) {
-            C* h = envo + (size_t)t * cl * cl + i0 * cl + j;
+            C* h = envo + ((size_t)t << (2 * lcl)) + (i0 << lcl) + j;
             h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
           }
         });
@@ -316,124 +348,91 @@ lr_sweep(Params p) {
   const int S = p.c.n_segments;
   if (item >= p.batch * S) return;
   const int b = item / S, g = item % S;
-  unsigned char* base = smem_raw + (size_t)team * p.L.team_bytes;
-  C* A = reinterpret_cast<C*>(base + p.L.a);
-  C* AH = reinterpret_cast<C*>(base + p.L.ah);
-  C* LAM = reinterpret_cast<C*>(base + p.L.env);
-  C* M = reinterpret_cast<C*>(base + p.L.m);
-  C* BR = reinterpret_cast<C*>(base + p.L.br);
-  C* PIN = reinterpret_cast<C*>(base + p.L.pin);
-  C* MR = reinterpret_cast<C*>(base + p.L.mr);
-  R* contrib = reinterpret_cast<R*>(base + p.L.contrib);
-  C* mres = reinterpret_cast<C*>(base + p.L.mres);
-  int* minfo = reinterpret_cast<int*>(base + p.L.minfo);
-  R* mps = reinterpret_cast<R*>(base + p.L.mps);
-  C* G = M;  // gradient cores alias the M slots (dead after the bracket stage)
+  TeamSmem<R> sm(smem_raw + (size_t)team * p.L.team_bytes, p.L);
+  const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
+  const R* coef_b = p.coef ? reinterpret_cast<const R*>(p.coef) + (int64_t)b * p.coef_stride : nullptr;
+  C* LAM = sm.ENV;
+  C* M = sm.M;
+  C* G = sm.M;  // gradient cores alias the M slots (dead after the bracket stage)
+  C* PIN = sm.PIN;
 
   const tq_segment seg = p.c.segs[g];
   const C* env_g = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
   R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
   if (tid == 0) LAM[0] = cmk<C>(R(1), R(0));
-  team_sync<TEAM>();
   for (int q = 0; q < seg.site_count; ++q) {
     const tq_site st = p.c.sites[seg.site_begin + q];
     const int cl = st.chi_l, cr = st.chi_r;
-    const int lcr = 31 - __clz(cr);
+    const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = p.mode == 0 ? st.rl_db : 1;
-    resolve_mats<R, TEAM>(p, st, b, tid, mres, minfo, mps);
+    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, false, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.sedge);
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
-      const int per = cr * cr;
-      for (int e = tid; e < npin * per; e += TEAM) {
-        const int ch = e / per, r = e % per;
+      const int lper = 2 * lcr;
+      for (int e = tid; e < (npin << lper); e += TEAM) {
+        const int ch = e >> lper, r = e & ((1 << lper) - 1);
         PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
       }
     }
     team_sync<TEAM>();
-    fold_site<R, LD, TEAM>(p, st, tid, mres, A, AH, lcr);
+    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
     team_sync<TEAM>();
     // M[a][s] = Lam[a] * A[s]
     gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cl, 1,
         [&](int t, int) { return LAM + (t >> 1) * MS; },
-        [&](int t, int) { return A + (t & 1) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-          C* o = M + t * MS + i0 * LD + j;
-          o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
-        });
+        [&](int t, int) { return sm.A + (t & 1) * MS; },
+        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     team_sync<TEAM>();
-    // BR[bb][s'] = sum over edges (a -> bb) of coef * O_{s's} M[a][s]
-    {
-      const int nel = db * 2 * cl * cr;
-      for (int e = tid; e < nel; e += TEAM) {
-        const int ij = e % (cl * cr);
-        const int bs = e / (cl * cr);
-        const int bb = bs >> 1, sp = bs & 1;
-        const int i = ij >> lcr, j = ij & (cr - 1);
-        C acc = cmk<C>(R(0), R(0));
-        for (int ei = 0; ei < st.lr_edge_count; ++ei) {
-          const tq_edge ed = p.c.edges[st.lr_edge_begin + ei];
-          if (ed.b != bb) continue;
-          const R cf = coef_at<R>(p, b, ed.coef);
-          const int s = pauli_src<C>(ed.op, sp);
-          const C f = pauli_fac<C>(ed.op, sp);
-          const C t = cmul(f, M[(ed.a * 2 + s) * MS + i * LD + j]);
-          acc.x += cf * t.x; acc.y += cf * t.y;
-        }
-        BR[(bb * 2 + sp) * MS + i * LD + j] = acc;
-      }
-    }
+    bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
     team_sync<TEAM>();
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
     gemm_group<C, LD, TEAM>(tid, db, cr, cr, cl, 2,
-        [&](int, int qq) { return AH + qq * MS; },
-        [&](int t, int qq) { return BR + (t * 2 + qq) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-          C* o = LAM + t * MS + i0 * LD + j;
-          o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
-        });
+        [&](int, int qq) { return sm.AH + qq * MS; },
+        [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
+        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     if (p.mode == 0) {
-      // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the BR stage)
+      // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
       gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
-          [&](int t, int qq) { return BR + (qq * 2 + t) * MS; },
+          [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
           [&](int, int qq) { return PIN + qq * MS; },
-          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-            C* o = G + t * MS + i0 * LD + j;
-            o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
-          });
+          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
-      // ---- column adjoint: per (alpha, beta) pair forward fold with checkpoints of the
-      // components projectors discard, then the backward walk accumulating Im<u, sigma v>.
+      // ---- column adjoint: per (alpha, beta) pair forward fold keeping the components
+      // projectors discard, then the backward walk accumulating Im<u, sigma v>.
       const int ntr = st.n_train;
+      R* contrib = sm.contrib;
       for (int t = 0; t < ntr; ++t) contrib[t * TEAM + tid] = R(0);
       const int npair = cl * cr;
+      const int nops = st.op_count;
       for (int pi = tid; pi < npair; pi += TEAM) {
         const int al = pi >> lcr, be = pi & (cr - 1);
-        if (!pass_ok(p, st, al, be)) continue;
+        if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
         C sv[MAXSAVE];
         int ns = 0;
         C v0 = cmk<C>(R(st.init[0]), R(st.init[1]));
         C v1 = cmk<C>(R(st.init[2]), R(st.init[3]));
-        for (int oi = 0; oi < st.op_count; ++oi) {
-          const tq_op op = p.c.ops[st.op_begin + oi];
-          const int e = op.lmat + op_digit(op, al, be);
-          const int cls = (minfo[e] >> 8) & 0xff;
+        for (int oi = 0; oi < nops; ++oi) {
+          const int c = sm.ocode[oi];
+          const int e = oc_lmat(c) + oc_digit(c, al, be);
+          const int cls = (sm.minfo[e] >> 8) & 0xff;
           if (cls == 1) sv[ns++] = v1;
           else if (cls == 2) sv[ns++] = v0;
           else if (cls == 3) { sv[ns++] = v0; sv[ns++] = v1; }
-          const C* Mm = mres + 4 * e;
+          const C* Mm = sm.mres + 4 * e;
           C n0 = cmul(Mm[0], v0); cfma(n0, Mm[1], v1);
           C n1 = cmul(Mm[2], v0); cfma(n1, Mm[3], v1);
           v0 = n0; v1 = n1;
         }
         C u0 = G[al * LD + be], u1 = G[MS + al * LD + be];
-        for (int oi = st.op_count - 1; oi >= 0; --oi) {
-          const tq_op op = p.c.ops[st.op_begin + oi];
-          const int e = op.lmat + op_digit(op, al, be);
-          const int info = minfo[e];
+        for (int oi = nops - 1; oi >= 0; --oi) {
+          const int c = sm.ocode[oi];
+          const int e = oc_lmat(c) + oc_digit(c, al, be);
+          const int info = sm.minfo[e];
           const int kind = info & 0xff, cls = (info >> 8) & 0xff;
-          if (op.tidx >= 0 && kind != 0) {
+          const int tix = oc_tidx(c);
+          if (tix >= 0 && kind != 0) {
             // Im<u, sigma v>, sigma = X (kind 1), Y (2), Z (3)
             C s0, s1;
             if (kind == 1) { s0 = v1; s1 = v0; }
@@ -441,25 +440,23 @@ lr_sweep(Params p) {
             else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
             C d = cmk<C>(R(0), R(0));
             cfmac(d, u0, s0); cfmac(d, u1, s1);
-            contrib[op.tidx * TEAM + tid] += d.y;
+            contrib[tix * TEAM + tid] += d.y;
           }
-          const C* Mm = mres + 4 * e;
-          // u <- M^H u
-          C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+          const C* Mm = sm.mres + 4 * e;
+          C w0 = cmk<C>(R(0), R(0)), w1 = w0;   // u <- M^H u
           cfmac(w0, Mm[0], u0); cfmac(w0, Mm[2], u1);
           cfmac(w1, Mm[1], u0); cfmac(w1, Mm[3], u1);
           u0 = w0; u1 = w1;
-          // v <- state before this op
-          if (cls == 0) {
+          if (cls == 0) {                        // v <- state before this op
             C x0 = cmk<C>(R(0), R(0)), x1 = x0;
             cfmac(x0, Mm[0], v0); cfmac(x0, Mm[2], v1);
             cfmac(x1, Mm[1], v0); cfmac(x1, Mm[3], v1);
             v0 = x0; v1 = x1;
           } else if (cls == 1) {
-            const R sc = R(1) / mps[e];
+            const R sc = sm.mps[e];
             v0 = cmk<C>(v0.x * sc, v0.y * sc); v1 = sv[--ns];
           } else if (cls == 2) {
-            const R sc = R(1) / mps[e];
+            const R sc = sm.mps[e];
             v1 = cmk<C>(v1.x * sc, v1.y * sc); v0 = sv[--ns];
           } else {
             v1 = sv[--ns]; v0 = sv[--ns];
@@ -471,14 +468,14 @@ lr_sweep(Params p) {
       {
         const int warp = tid >> 5, lane = tid & 31;
         constexpr int NW = TEAM / 32;
-        for (int oi = warp; oi < st.op_count; oi += NW) {
-          const tq_op op = p.c.ops[st.op_begin + oi];
-          if (op.tidx < 0) continue;
+        for (int oi = warp; oi < nops; oi += NW) {
+          const int tix = oc_tidx(sm.ocode[oi]);
+          if (tix < 0) continue;
           R s = R(0);
-          for (int k = lane; k < TEAM; k += 32) s += contrib[op.tidx * TEAM + k];
+          for (int k = lane; k < TEAM; k += 32) s += contrib[tix * TEAM + k];
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-          if (lane == 0) gpart[op.gidx] = s;
+          if (lane == 0) gpart[sm.ogidx[oi]] = s;
         }
       }
       team_sync<TEAM>();
@@ -487,27 +484,23 @@ lr_sweep(Params p) {
       gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cr, 1,
           [&](int t, int) { return M + t * MS; },
           [&](int, int) { return PIN; },
-          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-            C* o = MR + t * MS + i0 * LD + j;
-            o[0] = a0; if (rt > 1) o[LD] = a1; if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
-          });
+          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(sm.MR + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       if (st.fin_count > 0) {
         const int ncombo = da * 4;  // (a, s', s)
-        R* part = contrib;          // [2 * ncombo][TEAM] partial sums (re, im)
+        R* part = sm.contrib;       // [2 * ncombo][TEAM] partial sums (re, im)
         for (int cmb = 0; cmb < ncombo; ++cmb) {
           const int a = cmb >> 2, sp = (cmb >> 1) & 1, s = cmb & 1;
           C acc = cmk<C>(R(0), R(0));
           for (int e = tid; e < cl * cr; e += TEAM) {
-            const int i = e >> lcr, j = e & (cr - 1);
-            cfmac(acc, A[sp * MS + i * LD + j], MR[(a * 2 + s) * MS + i * LD + j]);
+            const int off = (e >> lcr) * LD + (e & (cr - 1));
+            cfmac(acc, sm.A[sp * MS + off], sm.MR[(a * 2 + s) * MS + off]);
           }
           part[(2 * cmb) * TEAM + tid] = acc.x;
           part[(2 * cmb + 1) * TEAM + tid] = acc.y;
         }
         team_sync<TEAM>();
-        // reduce and finalise (one warp, fixed order)
-        if (tid < 32) {
+        if (tid < 32) {  // reduce and finalise (one warp, fixed order)
           for (int fi = 0; fi < st.fin_count; ++fi) {
             const tq_edge fe = p.c.fins[st.fin_begin + fi];
             double vre = 0.0, vim = 0.0;
@@ -535,6 +528,71 @@ lr_sweep(Params p) {
       team_sync<TEAM>();
     }
   }
+}
+
+
+// ------------------------------------------------------------------ inner product sweep
+// out[b] = <bra(theta_bra_b) | ket(theta_ket_b)>: one left-to-right transfer with distinct
+// bra and ket columns, env L (chi_bra x chi_ket):  L' = sum_s Ab[s]^H (L Ak[s])  (tt_inner, tt.py:247-255).
+struct InnerParams {
+  tq_chain ket, bra;
+  int32_t batch;
+  const void* theta_ket; int64_t ket_stride;
+  const void* theta_bra; int64_t bra_stride;
+  double* out;
+  int32_t team_bytes;
+  int32_t off_ak, off_ahk, off_ab, off_ahb, off_t, off_l, off_mk, off_ik, off_pk, off_ok, off_gk, off_mb, off_ib, off_pb, off_ob, off_gb;
+};
+
+template <typename R, int CHI, int TEAM>
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM)
+inner_sweep(InnerParams p) {
+  using C = typename CT<R>::T;
+  constexpr int LD = CHI + 1;
+  constexpr int MS = LD * LD;
+  constexpr int TEAMS = TEAM == 32 ? 4 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int team = threadIdx.x / TEAM;
+  const int tid = threadIdx.x % TEAM;
+  const int b = blockIdx.x * TEAMS + team;
+  if (b >= p.batch) return;
+  unsigned char* base = smem_raw + (size_t)team * p.team_bytes;
+  C* Ak = reinterpret_cast<C*>(base + p.off_ak); C* AHk = reinterpret_cast<C*>(base + p.off_ahk);
+  C* Ab = reinterpret_cast<C*>(base + p.off_ab); C* AHb = reinterpret_cast<C*>(base + p.off_ahb);
+  C* T = reinterpret_cast<C*>(base + p.off_t); C* L = reinterpret_cast<C*>(base + p.off_l);
+  const R* thk = reinterpret_cast<const R*>(p.theta_ket) + (int64_t)b * p.ket_stride;
+  const R* thb = reinterpret_cast<const R*>(p.theta_bra) + (int64_t)b * p.bra_stride;
+  if (tid == 0) L[0] = cmk<C>(R(1), R(0));
+  const int n = p.ket.segs[0].site_count;
+  for (int q = 0; q < n; ++q) {
+    const tq_site sk = p.ket.sites[p.ket.segs[0].site_begin + q];
+    const tq_site sb = p.bra.sites[p.bra.segs[0].site_begin + q];
+    stage_site<R, TEAM>(p.ket, thk, nullptr, sk, tid, true, reinterpret_cast<C*>(base + p.off_mk),
+                        reinterpret_cast<int*>(base + p.off_ik), reinterpret_cast<R*>(base + p.off_pk),
+                        reinterpret_cast<int*>(base + p.off_ok), reinterpret_cast<int*>(base + p.off_gk), nullptr);
+    stage_site<R, TEAM>(p.bra, thb, nullptr, sb, tid, true, reinterpret_cast<C*>(base + p.off_mb),
+                        reinterpret_cast<int*>(base + p.off_ib), reinterpret_cast<R*>(base + p.off_pb),
+                        reinterpret_cast<int*>(base + p.off_ob), reinterpret_cast<int*>(base + p.off_gb), nullptr);
+    team_sync<TEAM>();
+    fold_site<R, LD, TEAM>(p.ket, sk, tid, reinterpret_cast<C*>(base + p.off_mk), reinterpret_cast<int*>(base + p.off_ok),
+                           Ak, AHk, 31 - __clz(sk.chi_r));
+    fold_site<R, LD, TEAM>(p.bra, sb, tid, reinterpret_cast<C*>(base + p.off_mb), reinterpret_cast<int*>(base + p.off_ob),
+                           Ab, AHb, 31 - __clz(sb.chi_r));
+    team_sync<TEAM>();
+    // T[s] = L * Ak[s]
+    gemm_group<C, LD, TEAM>(tid, 2, sb.chi_l, sk.chi_r, sk.chi_l, 1,
+        [&](int, int) { return L; },
+        [&](int t, int) { return Ak + t * MS; },
+        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(T + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+    team_sync<TEAM>();
+    // L' = sum_s AHb[s] T[s]
+    gemm_group<C, LD, TEAM>(tid, 1, sb.chi_r, sk.chi_r, sb.chi_l, 2,
+        [&](int, int qq) { return AHb + qq * MS; },
+        [&](int, int qq) { return T + qq * MS; },
+        [&](int, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(L + i0 * LD + j, rt, a0, a1, a2, a3); });
+    team_sync<TEAM>();
+  }
+  if (tid == 0) { p.out[2 * b] = double(L[0].x); p.out[2 * b + 1] = double(L[0].y); }
 }
 
 // ------------------------------------------------------------------ reductions
@@ -622,6 +680,9 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   off = align_up(off, 16);
   L.minfo = (int32_t)off; off += align_up((size_t)c->max_lmat * 4, 16);
   L.mps = (int32_t)off; off += align_up((size_t)c->max_lmat * rsz, 16);
+  L.ocode = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
+  L.ogidx = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
+  L.sedge = (int32_t)off; off += align_up((size_t)(c->max_edges > 0 ? c->max_edges : 1) * (rsz == 8 ? 24 : 16), 16);
   L.team_bytes = (int32_t)align_up(off, 128);
   return L;
 }
@@ -749,6 +810,47 @@ static tq_status values_impl(const tq_chain* c, int batch, const void* theta, in
   return TQ_OK;
 }
 
+
+template <typename R, int CHI>
+static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
+  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 256);
+  constexpr int TEAMS = TEAM == 32 ? 4 : 1;
+  const size_t csz = 2 * sizeof(R), ms = (size_t)(CHI + 1) * (CHI + 1) * csz;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const int32_t o = (int32_t)off; off = align_up(off + bytes, 16); return o; };
+  ip.off_ak = take(2 * ms); ip.off_ahk = take(2 * ms); ip.off_ab = take(2 * ms); ip.off_ahb = take(2 * ms);
+  ip.off_t = take(2 * ms); ip.off_l = take(ms);
+  ip.off_mk = take((size_t)ip.ket.max_lmat * 4 * csz); ip.off_ik = take((size_t)ip.ket.max_lmat * 4);
+  ip.off_pk = take((size_t)ip.ket.max_lmat * sizeof(R)); ip.off_ok = take((size_t)(ip.ket.max_ops + 1) * 4);
+  ip.off_gk = take((size_t)(ip.ket.max_ops + 1) * 4);
+  ip.off_mb = take((size_t)ip.bra.max_lmat * 4 * csz); ip.off_ib = take((size_t)ip.bra.max_lmat * 4);
+  ip.off_pb = take((size_t)ip.bra.max_lmat * sizeof(R)); ip.off_ob = take((size_t)(ip.bra.max_ops + 1) * 4);
+  ip.off_gb = take((size_t)(ip.bra.max_ops + 1) * 4);
+  ip.team_bytes = (int32_t)align_up(off, 128);
+  const size_t smem = (size_t)ip.team_bytes * TEAMS;
+  if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "inner product layout exceeds shared memory");
+  cudaFuncSetAttribute(inner_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  inner_sweep<R, CHI, TEAM><<<(ip.batch + TEAMS - 1) / TEAMS, TEAM * TEAMS, smem, s>>>(ip);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
+  return TQ_OK;
+}
+
+template <typename R>
+static tq_status inner_impl(InnerParams& ip, cudaStream_t s) {
+  const int chi = chi_bucket(ip.ket.chi_max > ip.bra.chi_max ? ip.ket.chi_max : ip.bra.chi_max);
+  switch (chi) {
+    case 2: return launch_inner<R, 2>(ip, s);
+    case 4: return launch_inner<R, 4>(ip, s);
+    case 8: return launch_inner<R, 8>(ip, s);
+    case 16: return launch_inner<R, 16>(ip, s);
+    case 32:
+      if (sizeof(R) == 8) return fail(TQ_ERR_UNSUPPORTED, "complex128 mode supports bond dimension <= 16");
+      return launch_inner<R, 32>(ip, s);
+    default: return fail(TQ_ERR_UNSUPPORTED, "bond dimension exceeds 32");
+  }
+}
+
 }  // namespace tq
 
 using namespace tq;
@@ -826,9 +928,18 @@ tq_status tq_ffma_peak(int32_t iters, void* stream, double* tflops_out) {
   return TQ_OK;
 }
 
-tq_status tq_inner(const tq_chain*, const void*, int64_t, const tq_chain*, const void*, int64_t, int32_t, int32_t,
-                   double*, void*) {
-  return fail(TQ_ERR_UNSUPPORTED, "tq_inner is not built in this version");
+tq_status tq_inner(const tq_chain* bra, const void* theta_bra, int64_t bra_stride, const tq_chain* ket,
+                   const void* theta_ket, int64_t ket_stride, int32_t dtype, int32_t batch, double* out, void* stream) {
+  if (!bra || !ket) return fail(TQ_ERR_INPUT, "null chain");
+  if (bra->n_segments != 1 || ket->n_segments != 1) return fail(TQ_ERR_INPUT, "inner product chains must have one segment");
+  if (batch <= 0) return TQ_OK;
+  InnerParams ip{};
+  ip.ket = *ket; ip.bra = *bra; ip.batch = batch;
+  ip.theta_ket = theta_ket; ip.ket_stride = ket_stride; ip.theta_bra = theta_bra; ip.bra_stride = bra_stride; ip.out = out;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == TQ_C64) return inner_impl<float>(ip, s);
+  if (dtype == TQ_C128) return inner_impl<double>(ip, s);
+  return fail(TQ_ERR_INPUT, "unknown dtype");
 }
 
 const char* tq_status_string(tq_status s) {
@@ -852,7 +963,7 @@ int32_t tq_abi_layout(int32_t* sizes, int32_t n) {
 }
 
 const char* tq_build_info(void) {
-  return "tq_engine sm_100a: rl_sweep/lr_sweep<float|double, chi 2..32>, reduce_energy, reduce_grad, ffma_probe";
+  return "tq_engine sm_100a: rl_sweep/lr_sweep<float|double, chi 2..32>, reduce_energy, reduce_grad, inner_sweep, ffma_probe";
 }
 
 }  // extern "C"

@@ -166,3 +166,20 @@ def check_residue(energy_full: torch.Tensor, im_extra, tol: float):
     worst = float(im.abs().max()) if im.numel() else 0.0
     if worst > tol:
         raise NonHermitianResidue(f"imaginary residue {worst:.3e} exceeds {tol:.0e}")
+
+
+def inner_raw(dp_bra: _lib.DevicePlan, theta_bra: torch.Tensor, dp_ket: _lib.DevicePlan, theta_ket: torch.Tensor,
+              dtype: str) -> torch.Tensor:
+    """<bra_b|ket_b> for b in the batch (complex128 [B]); plans compiled in 'state' mode."""
+    code, tdt = _dtype(dtype)
+    tb = theta_bra.to(device=dp_ket.device, dtype=tdt).contiguous()
+    tk = theta_ket.to(device=dp_ket.device, dtype=tdt).contiguous()
+    B = tk.shape[0]
+    if tb.shape[0] != B:
+        raise InputError("bra and ket batches differ")
+    out = torch.zeros(B, 2, dtype=torch.float64, device=dp_ket.device)
+    st = _lib.load().tq_inner(ctypes.byref(dp_bra.chain), tb.data_ptr(), tb.stride(0) if tb.numel() else 0,
+                              ctypes.byref(dp_ket.chain), tk.data_ptr(), tk.stride(0) if tk.numel() else 0,
+                              code, B, out.data_ptr(), _stream())
+    _lib.check(st)
+    return torch.view_as_complex(out)

@@ -102,3 +102,7 @@ class EngineUnavailable(NumericalError):
 
 class EngineError(NumericalError):
     """A CUDA launch or runtime call failed inside the engine."""
+
+
+class TooManyVertices(InputError):
+    """Brute force enumeration is capped; the graph is too big."""

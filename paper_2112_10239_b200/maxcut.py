@@ -1,0 +1,377 @@
+"""MaxCut through the multi-basis encoding (MBE), on the B200 engine.
+
+Mirrors ``tnsim.maxcut`` (reference ``maxcut.py:39-319``).  Vertex 2k is read out
+as <Z_k>, vertex 2k+1 as <X_k> (single-site readouts, ``maxcut.py:127-135``); the
+relaxed loss is ``L = sum_(u,v,w) w tanh(a<s_u>) tanh(a<s_v>)`` (``maxcut.py:219-252``).
+
+Device path per optimiser step, for B restarts at once (the reference's thread
+pool over restarts, ``maxcut.py:309-313``, becomes the batch dimension):
+  values sweep   -> readouts r[B, V]                     (tq_term_values)
+  torch          -> t = tanh(a r), loss, cotangents g_v = a (1 - t_v^2) sum_nbr w t_u
+  energy sweep   -> grad[B, P] with per-restart coefficients g (tq_energy_grad)
+  torch          -> Adam update (reference autodiff.py:650-658)
+Neighbour sums use padded adjacency lists (gather + fixed-order sum, no atomics),
+so results are bit-identical run to run.  Final readouts for the sign rounding use
+the complex128 kernels so cuts are bit-exact whenever the readout margin exceeds 1e-9.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import chain as C
+from . import engine as E
+from .autodiff import _check_engine, _device, init_params
+from .circuits import Circuit, standard_gate
+from .errors import (
+    DivergenceDetected,
+    DuplicateEdge,
+    InputError,
+    InvalidLabel,
+    ParseError,
+    SelfLoop,
+    SizeMismatch,
+    TooManyVertices,
+)
+from .hamiltonians import PauliHamiltonian, PauliTerm
+from .seeding import spawn
+
+MAX_BRUTE_FORCE_VERTICES = 22
+
+
+@dataclass(frozen=True)
+class Graph:
+    """Undirected weighted graph on vertices 0..num_vertices-1 (reference maxcut.py:39-79)."""
+
+    num_vertices: int
+    edges: tuple = ()
+
+    def __post_init__(self):
+        if isinstance(self.num_vertices, bool) or not isinstance(self.num_vertices, (int, np.integer)):
+            raise InputError("num_vertices must be an integer")
+        if self.num_vertices < 0:
+            raise InputError("num_vertices must be non-negative")
+        out, seen = [], set()
+        for e in self.edges:
+            if len(e) != 3:
+                raise InputError(f"edge {e!r} is not a (u, v, weight) triple")
+            u, v, w = e
+            if isinstance(u, bool) or isinstance(v, bool) or not isinstance(u, (int, np.integer)) \
+                    or not isinstance(v, (int, np.integer)):
+                raise InvalidLabel("vertex labels must be integers")
+            u, v, w = int(u), int(v), float(w)
+            if not (0 <= u < self.num_vertices and 0 <= v < self.num_vertices):
+                raise InvalidLabel(f"edge ({u}, {v}) references a vertex outside 0..{self.num_vertices - 1}")
+            if u == v:
+                raise SelfLoop(f"vertex {u} connected to itself")
+            if not math.isfinite(w):
+                raise InputError(f"edge ({u}, {v}) has non-finite weight")
+            key = (min(u, v), max(u, v))
+            if key in seen:
+                raise DuplicateEdge(f"edge ({u}, {v}) listed twice")
+            seen.add(key)
+            out.append((u, v, w))
+        object.__setattr__(self, "num_vertices", int(self.num_vertices))
+        object.__setattr__(self, "edges", tuple(out))
+
+    @property
+    def total_abs_weight(self) -> float:
+        return float(sum(abs(w) for _, _, w in self.edges))
+
+
+def load_graph(text: str) -> Graph:
+    """Edge-list parser (reference maxcut.py:82-124)."""
+    header, raw, first = None, [], True
+    for lineno, line in enumerate(text.splitlines(), start=1):
+        body = line.split("#", 1)[0].strip()
+        if not body:
+            continue
+        fields = body.split()
+        if first and len(fields) == 1:
+            try:
+                header = int(fields[0])
+            except ValueError:
+                raise ParseError(f"line {lineno}: expected an integer header, got {body!r}")
+            if header < 0:
+                raise ParseError(f"line {lineno}: vertex count must be non-negative")
+            first = False
+            continue
+        first = False
+        if len(fields) not in (2, 3):
+            raise ParseError(f"line {lineno}: expected 'u v [w]', got {body!r}")
+        try:
+            u, v = int(fields[0]), int(fields[1])
+        except ValueError:
+            raise ParseError(f"line {lineno}: vertex labels must be integers, got {body!r}")
+        if u < 0 or v < 0:
+            raise ParseError(f"line {lineno}: vertex labels must be non-negative")
+        w = 1.0
+        if len(fields) == 3:
+            try:
+                w = float(fields[2])
+            except ValueError:
+                raise ParseError(f"line {lineno}: weight must be a number, got {fields[2]!r}")
+        raw.append((u, v, w))
+    n = header if header is not None else (1 + max(max(u, v) for u, v, _ in raw) if raw else 0)
+    return Graph(n, tuple(raw))
+
+
+def pairing_graph(num_vertices: int, degree: int, rng) -> Graph:
+    """Random simple d-regular graph by the pairing model (SURVEY.md section 8d cfg3 spec)."""
+    while True:
+        stubs = np.repeat(np.arange(num_vertices), degree)
+        rng.shuffle(stubs)
+        pairs = stubs.reshape(-1, 2)
+        keys = {(min(u, v), max(u, v)) for u, v in pairs}
+        if all(u != v for u, v in pairs) and len(keys) == len(pairs):
+            return Graph(num_vertices, tuple((int(u), int(v), 1.0) for u, v in pairs))
+
+
+def mbe_encode(graph: Graph):
+    """(n_qubits, [(qubit, 'Z'|'X') per vertex]) (reference maxcut.py:127-135)."""
+    n = (graph.num_vertices + 1) // 2
+    return n, tuple((v // 2, "Z" if v % 2 == 0 else "X") for v in range(graph.num_vertices))
+
+
+def mbe_loss(t_vals, graph: Graph) -> float:
+    """Reference maxcut.py:138-145."""
+    t = np.asarray(t_vals, dtype=float).reshape(-1)
+    if t.size != graph.num_vertices:
+        raise SizeMismatch(f"{t.size} values supplied for a graph with {graph.num_vertices} vertices")
+    return float(sum(w * t[u] * t[v] for u, v, w in graph.edges))
+
+
+def round_cut(expectations) -> tuple:
+    """Sign rounding, 0 -> +1 (reference maxcut.py:148-153)."""
+    x = np.asarray(expectations, dtype=float).reshape(-1)
+    if x.size and not np.all(np.isfinite(x)):
+        raise InputError("expectations must be finite")
+    return tuple(1 if v >= 0 else -1 for v in x)
+
+
+def cut_value(graph: Graph, assignment) -> float:
+    """Reference maxcut.py:156-164."""
+    a = np.asarray(assignment).reshape(-1)
+    if a.size != graph.num_vertices:
+        raise SizeMismatch(f"assignment length {a.size} does not match {graph.num_vertices} vertices")
+    if not all(v in (-1, 1) for v in a.tolist()):
+        raise InvalidLabel("assignment entries must be +1 or -1")
+    return float(sum(w * (1 - int(a[u]) * int(a[v])) / 2 for u, v, w in graph.edges))
+
+
+def brute_force_maxcut(graph: Graph):
+    """Exhaustive optimum with vertex 0 fixed (reference maxcut.py:167-183); V <= 22."""
+    nv = graph.num_vertices
+    if nv > MAX_BRUTE_FORCE_VERTICES:
+        raise TooManyVertices(f"{nv} vertices exceeds the brute-force limit of {MAX_BRUTE_FORCE_VERTICES}")
+    if nv == 0:
+        return 0.0, ()
+    pats = np.arange(1 << (nv - 1), dtype=np.uint32)
+    cuts = np.zeros(pats.shape)
+    for u, v, w in graph.edges:
+        bu = (pats >> (u - 1)) & 1 if u > 0 else np.zeros_like(pats)
+        bv = (pats >> (v - 1)) & 1 if v > 0 else np.zeros_like(pats)
+        cuts += w * (bu ^ bv)
+    best = int(np.argmax(cuts))
+    return float(cuts[best]), (1,) + tuple(-1 if (best >> (v - 1)) & 1 else 1 for v in range(1, nv))
+
+
+def brickwork_ansatz(n_qubits: int, depth: int = 4) -> Circuit:
+    """ry+rz rows separated by cz lines with alternating offset (reference maxcut.py:186-203)."""
+    if n_qubits < 1:
+        raise InputError("ansatz needs at least one qubit")
+    if depth < 1:
+        raise InputError("depth must be at least 1")
+    gates, train = [], []
+    for layer in range(depth):
+        for name in ("ry", "rz"):
+            for q in range(n_qubits):
+                train.append(len(gates))
+                gates.append(standard_gate(name, (q,), 0.0))
+        if layer < depth - 1:
+            for q in range(layer % 2, n_qubits - 1, 2):
+                gates.append(standard_gate("cz", (q, q + 1)))
+    return Circuit(n_qubits, tuple(gates), tuple(train))
+
+
+def _readout_terms(graph: Graph):
+    n, mapping = mbe_encode(graph)
+    return n, PauliHamiltonian(max(n, 1), tuple(PauliTerm(1.0, ((q, letter),)) for q, letter in mapping))
+
+
+class MBEObjective:
+    """Batched device objective: theta [B, P] -> (loss [B], grad [B, P]) on the GPU."""
+
+    def __init__(self, circuit: Circuit, graph: Graph, alpha: float = 1.0, *, dtype: str = "complex64",
+                 device=None, batch: int = 1, segments=None):
+        n, ham = _readout_terms(graph)
+        if circuit.n_qubits != n:
+            raise SizeMismatch(f"circuit has {circuit.n_qubits} qubits, encoding needs {n}")
+        if not math.isfinite(alpha) or alpha <= 0:
+            raise InputError("alpha must be positive and finite")
+        self.circuit, self.graph, self.alpha, self.dtype = circuit, graph, float(alpha), dtype
+        self.device = _device(device)
+        terms = C.normalize_terms(ham)
+        self.dp_values = E.device_plan(circuit, terms, "values", batch, self.device, segments, dtype=dtype)
+        self.dp_energy = E.device_plan(circuit, terms, "energy", batch, self.device, segments, dtype=dtype)
+        V = graph.num_vertices
+        deg = np.zeros(V, dtype=np.int64)
+        for u, v, _ in graph.edges:
+            deg[u] += 1
+            deg[v] += 1
+        md = int(deg.max()) if V and len(graph.edges) else 1
+        nbr = np.full((V, md), V, dtype=np.int64)   # index V = padding slot holding t = 0
+        wts = np.zeros((V, md))
+        fill = np.zeros(V, dtype=np.int64)
+        for u, v, w in graph.edges:
+            nbr[u, fill[u]], wts[u, fill[u]] = v, w
+            nbr[v, fill[v]], wts[v, fill[v]] = u, w
+            fill[u] += 1
+            fill[v] += 1
+        tdt = E.DTYPES[dtype][1]
+        self.nbr = torch.tensor(nbr, device=self.device)
+        self.wts = torch.tensor(wts, dtype=torch.float64, device=self.device)
+        eu = np.array([e[0] for e in graph.edges], dtype=np.int64)
+        ev = np.array([e[1] for e in graph.edges], dtype=np.int64)
+        self.eu = torch.tensor(eu, device=self.device)
+        self.ev = torch.tensor(ev, device=self.device)
+        self.ew = torch.tensor([e[2] for e in graph.edges], dtype=torch.float64, device=self.device)
+        self.tdt = tdt
+
+    def readouts(self, theta: torch.Tensor, dtype: str | None = None) -> torch.Tensor:
+        """Re<sigma_v> [B, V] (float64)."""
+        dt = dtype or self.dtype
+        dp = self.dp_values if dt == self.dtype else E.device_plan(
+            self.circuit, C.normalize_terms(_readout_terms(self.graph)[1]), "values", theta.shape[0],
+            self.device, None, dtype=dt)
+        return E.values_raw(dp, theta, dt).real
+
+    def __call__(self, theta: torch.Tensor):
+        r = self.readouts(theta)                                  # [B, V] float64
+        t = torch.tanh(self.alpha * r)
+        loss = (self.ew * t[:, self.eu] * t[:, self.ev]).sum(dim=1)
+        tp = torch.cat([t, torch.zeros(t.shape[0], 1, dtype=t.dtype, device=t.device)], dim=1)
+        nsum = (tp[:, self.nbr] * self.wts).sum(dim=2)             # sum_nbr w t_u   [B, V]
+        g = self.alpha * (1.0 - t * t) * nsum
+        _, grad = E.energy_grad_raw(self.dp_energy, theta, g, True, self.dtype)
+        return loss, grad
+
+
+def vertex_expectations(circuit: Circuit, theta, graph: Graph, engine: str = "tt", eps: float = 0.0,
+                        chi_max=None, *, dtype: str = "complex128", device=None):
+    """Per-vertex readouts (reference maxcut.py:206-216); complex128 by default for exact rounding."""
+    _check_engine(engine)
+    n, ham = _readout_terms(graph)
+    if circuit.n_qubits != n:
+        raise SizeMismatch(f"circuit has {circuit.n_qubits} qubits, encoding needs {n}")
+    th = np.asarray(theta, dtype=float)
+    single = th.ndim == 1
+    th2 = th.reshape(1, -1) if single else th
+    dev = _device(device)
+    dp = E.device_plan(circuit, C.normalize_terms(ham), "values", th2.shape[0], dev, None, dtype=dtype)
+    vals = E.values_raw(dp, torch.tensor(th2, dtype=E.DTYPES[dtype][1], device=dev), dtype).real.cpu().numpy()
+    return vals[0] if single else vals
+
+
+def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: str = "tt", eps: float = 0.0,
+                  chi_max=None, *, dtype: str = "complex64", device=None):
+    """fun(theta) -> (loss, grad) (reference maxcut.py:219-252), one device round trip per call."""
+    _check_engine(engine)
+    obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device)
+
+    def fun(theta):
+        th = torch.tensor(np.asarray(theta, dtype=float).reshape(1, -1), dtype=obj.tdt, device=obj.device)
+        loss, grad = obj(th)
+        return float(loss[0]), grad[0].double().cpu().numpy()
+
+    return fun
+
+
+@dataclass(frozen=True)
+class MbeResult:
+    assignment: tuple
+    cut_value: float
+    relaxed_loss: float
+    iterations: int
+    restart_index: int
+    seed: int
+
+
+def adam_batched(obj: MBEObjective, theta0: np.ndarray, rate: float, max_iters: int, tol: float = 1e-8,
+                 betas=(0.9, 0.999), adam_eps: float = 1e-8, optimizer: str = "adam"):
+    """Per-restart minimise (reference autodiff.py:614-659) with restarts as the batch.
+
+    Each restart stops on its own when its gradient norm drops below ``tol``
+    (frozen thereafter), exactly like independent reference runs."""
+    dev = obj.device
+    theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
+    B = theta.shape[0]
+    m = torch.zeros_like(theta)
+    v = torch.zeros_like(theta)
+    active = torch.ones(B, dtype=torch.bool, device=dev)
+    value = torch.zeros(B, dtype=torch.float64, device=dev)
+    iters = torch.zeros(B, dtype=torch.int64, device=dev)
+    b1, b2 = betas
+    for it in range(max_iters + 1):
+        loss, grad = obj(theta.to(obj.tdt))
+        grad = grad.double()
+        if not bool(torch.isfinite(loss).all()) or not bool(torch.isfinite(grad).all()):
+            raise DivergenceDetected(f"non-finite objective at iteration {it}")
+        value = torch.where(active, loss, value)
+        iters = torch.where(active, torch.full_like(iters, it), iters)
+        gnorm = torch.linalg.vector_norm(grad, dim=1)
+        active = active & (gnorm >= tol)
+        if it == max_iters or not bool(active.any()):
+            break
+        if optimizer == "gd":
+            upd = rate * grad
+        else:
+            m = torch.where(active[:, None], b1 * m + (1 - b1) * grad, m)
+            v = torch.where(active[:, None], b2 * v + (1 - b2) * grad * grad, v)
+            mhat = m / (1 - b1 ** (it + 1))
+            vhat = v / (1 - b2 ** (it + 1))
+            upd = rate * mhat / (torch.sqrt(vhat) + adam_eps)
+        theta = torch.where(active[:, None], theta - upd, theta)
+    return theta.cpu().numpy(), value.cpu().numpy(), iters.cpu().numpy()
+
+
+def solve_maxcut(graph: Graph, depth: int = 4, engine: str = "tt", eps: float = 0.0, chi_max=None,
+                 optimizer: str = "adam", rate: float = 0.1, restarts: int = 5, max_iters: int = 300,
+                 seed: int = 0, alpha: float = 1.0, threads: int = 1, *, dtype: str = "complex64", device=None):
+    """Train the brickwork ansatz, round to a cut (reference maxcut.py:273-319).
+
+    All restarts advance together as one batch; ``threads`` is accepted for API
+    compatibility (the batch replaces the reference's thread pool)."""
+    _check_engine(engine)
+    if optimizer not in ("gd", "adam"):
+        raise InputError(f"unknown optimizer {optimizer!r}")
+    if restarts < 1:
+        raise InputError("need at least one restart")
+    if graph.num_vertices == 0 or not graph.edges:
+        return MbeResult((1,) * graph.num_vertices, 0.0, 0.0, 0, 0, seed)
+    n, _ = mbe_encode(graph)
+    circuit = brickwork_ansatz(n, depth)
+    obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device, batch=restarts)
+    theta0 = np.stack([init_params(circuit.n_params, rng) for rng in spawn(seed, restarts)])
+    theta, loss, iters = adam_batched(obj, theta0, rate, max_iters, optimizer=optimizer)
+    exps = vertex_expectations(circuit, theta, graph, device=obj.device)
+    outcomes = []
+    for r in range(restarts):
+        asg = round_cut(exps[r])
+        outcomes.append((asg, cut_value(graph, asg), float(loss[r]), int(iters[r])))
+    best = 0
+    for r in range(1, restarts):
+        if outcomes[r][1] > outcomes[best][1]:
+            best = r
+    asg, cut, lval, it = outcomes[best]
+    return MbeResult(asg, cut, lval, it, best, seed)
+
+
+def result_to_dict(result: MbeResult, optimal=None) -> dict:
+    return {"cut": result.cut_value, "optimal": None if optimal is None else float(optimal),
+            "assignment": list(result.assignment), "loss": result.relaxed_loss, "iters": result.iterations,
+            "seed": result.seed}

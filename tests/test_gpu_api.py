@@ -1,0 +1,132 @@
+"""GPU tests of the wider API surface: MBE MaxCut (cfg3), inner products,
+product-state inputs, tlquantum-style TTCircuit, residue checks."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+from conftest import ocircuit  # noqa: E402
+from helpers_engine import grad_ok64, to_circuit  # noqa: E402
+from paper_2112_10239_b200 import autodiff as AD  # noqa: E402
+from paper_2112_10239_b200 import maxcut as MC  # noqa: E402
+from paper_2112_10239_b200 import tlq  # noqa: E402
+from paper_2112_10239_b200.errors import NonHermitianResidue, SizeMismatch  # noqa: E402
+from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, term, tfim  # noqa: E402
+from paper_2112_10239_b200.workloads import layered_circuit, theta_sets  # noqa: E402
+
+
+def test_mbe_objective_matches_reference(golden_small):
+    d = golden_small["mbe10"]
+    g = MC.Graph(10, tuple(tuple(e) for e in d["edges"]))
+    c = MC.brickwork_ansatz(5, d["depth"])
+    th = np.array(d["theta"])
+    for dtype, tol in (("complex128", 1e-10), ("complex64", 2e-5)):
+        loss, grad = MC.mbe_objective(c, g, alpha=d["alpha"], dtype=dtype)(th)
+        assert abs(loss - d["loss"]) < tol * max(1, abs(d["loss"])), dtype
+        assert np.max(np.abs(grad - np.array(d["grad"]))) < tol * max(1, np.max(np.abs(d["grad"]))), dtype
+    ev = MC.vertex_expectations(c, th, g)
+    np.testing.assert_allclose(ev, d["vertex"], atol=1e-12)
+    asg = MC.round_cut(ev)
+    assert list(asg) == d["assignment"] and MC.cut_value(g, asg) == d["cut"]
+
+
+def test_mbe_cfg3_bit_exact_cut(golden_large):
+    pairs = golden_large["cfg3_edges"]
+    g = MC.Graph(2048, tuple((int(u), int(v), 1.0) for u, v in pairs))
+    c = MC.brickwork_ansatz(1024, 4)
+    th = golden_large["cfg3_theta"]
+    ev = MC.vertex_expectations(c, th, g)  # complex128 readouts
+    np.testing.assert_allclose(ev, golden_large["cfg3_vertex"], atol=1e-11)
+    asg = np.array(MC.round_cut(ev), dtype=np.int8)
+    np.testing.assert_array_equal(asg, golden_large["cfg3_assignment"])
+    assert MC.cut_value(g, asg) == float(golden_large["cfg3_cut"])
+    loss, grad = MC.mbe_objective(c, g)(th)
+    ref = float(golden_large["cfg3_loss"])
+    assert abs(loss - ref) < 1e-5 * max(1.0, abs(ref))
+    assert grad_ok64(grad, golden_large["cfg3_grad"])
+
+
+def test_solve_maxcut_small_graphs():
+    tri = MC.Graph(3, ((0, 1, 1.0), (1, 2, 1.0), (0, 2, 1.0)))
+    assert MC.solve_maxcut(tri, restarts=3, max_iters=80, seed=1).cut_value == 2.0
+    c4 = MC.Graph(4, ((0, 1, 1.0), (1, 2, 1.0), (2, 3, 1.0), (3, 0, 1.0)))
+    assert MC.solve_maxcut(c4, restarts=3, max_iters=80, seed=1).cut_value == 4.0
+    a = MC.solve_maxcut(c4, restarts=2, max_iters=30, seed=7)
+    b = MC.solve_maxcut(c4, restarts=2, max_iters=30, seed=7, threads=2)
+    assert a == b
+
+
+def test_inner_product_matches_reference(golden_small):
+    d = golden_small["inner8"]
+    c = to_circuit(d["circuit"])
+    for dtype, tol in (("complex128", 1e-12), ("complex64", 2e-6)):
+        ip = AD.state_inner_product(c, d["theta_b"], c, d["theta_a"], dtype=dtype)
+        assert abs(ip - complex(d["re"], d["im"])) < tol, dtype
+
+
+def test_product_state_inputs_against_oracle():
+    rng = np.random.default_rng(5)
+    n = 6
+    vecs = rng.normal(size=(n, 2)) + 1j * rng.normal(size=(n, 2))
+    vecs /= np.linalg.norm(vecs, axis=1, keepdims=True)
+    c = layered_circuit(n, 6, "ry", "cz")
+    th = theta_sets(c.n_params, 1, seed=3)[0]
+    oc = O.ry_cz_layers(n, 6)
+    ov, og = O.grad_expval_tt(oc, O.tfim_terms(n), th, init_vectors=vecs)
+    circ = tlq.ansatz(n, 6, dtype="complex128")
+    with torch.no_grad():
+        for p, t in zip(circ._params, th):
+            p.fill_(float(t))
+    state = tlq.ProductState(vecs)
+    e = circ.forward_expectation_value(state, tfim(n))
+    e.backward()
+    g = np.array([float(p.grad) for p in circ._params])
+    assert abs(float(e) - ov) < 1e-10
+    np.testing.assert_allclose(g, og, atol=1e-10)
+    # <compare|U|state> for product states against the dense oracle
+    psi = O.simulate_dense(oc, th).reshape(-1)
+    comp = tlq.spins_to_tt_state([1, 0, 1, 1, 0, 0])
+    idx = int("101100", 2)
+    ip = circ.state_inner_product(tlq.spins_to_tt_state([0] * n), comp)
+    assert abs(ip - psi[idx]) < 1e-12
+
+
+def test_ttcircuit_matches_reference_circuit(golden_small):
+    circ = tlq.ansatz(10, 4, rot="y", ent="cnot")
+    case = golden_small["cases"][0]
+    with torch.no_grad():
+        for p, t in zip(circ._params, case["theta"]):
+            p.fill_(float(t))
+    assert circ.to_circuit().structure_key() == to_circuit(case["circuit"]).structure_key()
+    e = circ.forward_expectation_value(tlq.spins_to_tt_state([0] * 10), tlq.ising_hamiltonian(10))
+    e.backward()
+    assert abs(float(e) - case["value"]) < 1e-5 * max(1, abs(case["value"]))
+    g = np.array([float(p.grad) for p in circ._params])
+    assert grad_ok64(g, case["grad"])
+
+
+def test_non_hermitian_residue_raises():
+    c = layered_circuit(4, 3)
+    th = theta_sets(c.n_params, 1, seed=2)[0]
+    ham = PauliHamiltonian(4, (term(1.0 + 0.3j, {0: "Z"}),))
+    with pytest.raises(NonHermitianResidue):
+        AD.evaluate_expval(c, ham, th)
+    with pytest.raises(SizeMismatch):
+        MC.mbe_objective(MC.brickwork_ansatz(3, 2), MC.Graph(3, ((0, 1, 1.0),)))
+
+
+def test_expectation_values_batched_against_oracle():
+    c = layered_circuit(12, 8, "rx", "cz")
+    th = theta_sets(c.n_params, 3, seed=8)
+    groups = [{0: "X"}, {5: "Y", 6: "Z"}, {2: "Z", 9: "X"}]
+    vals = AD.expectation_values(c, th, groups, dtype="complex128")
+    oc = O.ry_cz_layers(12, 8, "rx", "cz")
+    for b in range(3):
+        ref = O.taped_term_values(oc, th[b], [tuple(sorted(g.items())) for g in groups])
+        np.testing.assert_allclose(vals[b], ref, atol=1e-12)

@@ -112,3 +112,11 @@ def test_theta_sets_are_float32_exact():
     np.testing.assert_array_equal(th, th.astype(np.float32).astype(np.float64))
     g = np.array(O.generator(0).uniform(-np.pi, np.pi, 500))
     np.testing.assert_array_equal(theta_sets(500, 1, seed=0)[0], g.astype(np.float32).astype(np.float64))
+
+
+def test_every_module_imports_without_a_gpu():
+    import importlib
+
+    for m in ("autodiff", "chain", "circuits", "engine", "errors", "hamiltonians", "maxcut", "program",
+              "roofline", "seeding", "tlq", "workloads", "_lib", "build"):
+        importlib.import_module(f"paper_2112_10239_b200.{m}")
