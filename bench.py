@@ -376,13 +376,186 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- cfg3 (MBE MaxCut)
+def cfg3_problem():
+    from paper_2112_10239_b200 import maxcut as MC
+    from paper_2112_10239_b200.seeding import generator
+
+    rng = generator(3)
+    graph = MC.pairing_graph(2048, 3, rng)
+    circuit = MC.brickwork_ansatz(1024, 4)
+    return MC, graph, circuit, rng
+
+
+def _mbe_oracle_step(args):
+    edges, theta = args
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    import oracle as O
+
+    t0 = time.perf_counter()
+    O.mbe_objective(O.brickwork(1024, 4), 2048, edges)(theta)
+    return time.perf_counter() - t0
+
+
+def run_cfg3(args, cfg):
+    """One Adam step (readouts -> tanh loss -> cotangents -> gradient sweep -> update) for
+    B restarts at once; metric = restart-steps (loss+gradient evaluations) per second."""
+    import ctypes
+
+    import torch
+
+    from paper_2112_10239_b200 import _lib, engine as E, roofline
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    MC, graph, circuit, rng = cfg3_problem()
+    B = args.batch or cfg.batch
+    from paper_2112_10239_b200.seeding import spawn
+    from paper_2112_10239_b200.workloads import f32
+
+    theta0 = np.stack([f32(r.uniform(-np.pi, np.pi, circuit.n_params)) for r in spawn(3 + rank, B)])
+    obj = MC.MBEObjective(circuit, graph, 1.0, device=dev, batch=B)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+    theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
+    m = torch.zeros_like(theta)
+    v = torch.zeros_like(theta)
+    ms_k = (ctypes.c_float * 2)()
+    dpe = obj.dp_energy
+    ws_buf, ws_bytes = dpe.workspace(B, _lib.TQ_FLAG_GRAD, _lib.TQ_C64, stream.cuda_stream)
+    energy = torch.empty(B, 2, dtype=torch.float64, device=dev)
+    grad = torch.empty(B, circuit.n_params, dtype=torch.float32, device=dev)
+    kt = {"values": [], "rl": [], "lr": []}
+
+    def step(it, timed=False):
+        nonlocal theta, m, v
+        th32 = theta.to(torch.float32)
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        r = E.values_raw(obj.dp_values, th32, "complex64").real
+        if timed:
+            b.record(stream)
+        t = torch.tanh(obj.alpha * r)
+        tp = torch.cat([t, torch.zeros(B, 1, dtype=t.dtype, device=dev)], dim=1)
+        g = (obj.alpha * (1.0 - t * t) * (tp[:, obj.nbr] * obj.wts).sum(dim=2)).to(torch.float32).contiguous()
+        fn = lib.tq_energy_grad_timed if timed else lib.tq_energy_grad
+        extra = (ms_k,) if timed else ()
+        _lib.check(fn(ctypes.byref(dpe.chain), _lib.TQ_C64, B, th32.data_ptr(), th32.stride(0), g.data_ptr(),
+                      g.stride(0), energy.data_ptr(), grad.data_ptr(), ws_buf.data_ptr(), ws_bytes,
+                      stream.cuda_stream, *extra))
+        gd = grad.double()
+        m = 0.9 * m + 0.1 * gd
+        v = 0.999 * v + 0.001 * gd * gd
+        theta = theta - 0.1 * (m / (1 - 0.9 ** (it + 1))) / (torch.sqrt(v / (1 - 0.999 ** (it + 1))) + 1e-8)
+        if timed:
+            b.synchronize()
+            kt["values"].append(a.elapsed_time(b))
+            kt["rl"].append(ms_k[0])
+            kt["lr"].append(ms_k[1])
+
+    for it in range(max(3, args.warmup)):
+        step(it)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.25)
+    times = []
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(k, timed=True)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    ms = sum(times) / len(times)
+    value = B * ws / (ms * 1e-3)
+    # e2e: host theta in, host loss/grad out, through the public objective
+    fun = MC.mbe_objective(circuit, graph, device=dev)
+    host = theta0[0]
+    for _ in range(2):
+        fun(host)
+    et = []
+    for _ in range(max(3, args.steps // 2)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fun(host)
+        e1.record(stream)
+        e1.synchronize()
+        et.append(e0.elapsed_time(e1))
+    e2e = 1.0 / (statistics.mean(et) * 1e-3)
+    if rank != 0:
+        return
+    ffma = ctypes.c_double(0)
+    _lib.check(lib.tq_ffma_peak(20000, stream.cuda_stream, ctypes.byref(ffma)))
+    from paper_2112_10239_b200 import chain as C
+
+    terms = C.normalize_terms(MC._readout_terms(graph)[1])
+    pe = roofline.eval_model(C.compile_chain(circuit, terms, "energy", segments=1), grad=True)
+    pv = roofline.eval_model(C.compile_chain(circuit, terms, "values", segments=1), grad=True)
+    cand = {"values_sweeps (rl+lr values)": (statistics.mean(kt["values"]), (pv["flops_rl"] + pv["flops_lr"]) * B),
+            "rl_sweep (cotangent-weighted)": (statistics.mean(kt["rl"]), pe["flops_rl"] * B),
+            "lr_sweep (gradient)": (statistics.mean(kt["lr"]), pe["flops_lr"] * B)}
+    kname = max(cand, key=lambda k: cand[k][0])
+    kms, kfl = cand[kname]
+    achieved = kfl / (kms * 1e-3) / 1e12
+    cpu = None
+    if not args.no_cpu_baseline:
+        import multiprocessing as mp
+
+        cores = host_cores()
+        nsamp = max(2, min(cores, 16))
+        jobs = [(list(graph.edges), theta0[i % B]) for i in range(nsamp)]
+        with mp.get_context("fork").Pool(min(cores, nsamp)) as pool:
+            t0 = time.perf_counter()
+            per = pool.map(_mbe_oracle_step, jobs)
+            wall = time.perf_counter() - t0
+        cpu = {"value": nsamp / wall, "unit": "evals/s", "cores": min(cores, nsamp), "kind": "port",
+               "sample": f"{nsamp} MBE objective evaluations (oracle port of tnsim mbe_objective, eps=0), "
+                         f"{sum(per):.1f} CPU-s"}
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    byts = (pe["bytes"] + pv["bytes"]) * B
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic pairing-model 3-regular graph (seed 3), seeded angles",
+        "config": {"workload": f"cfg3: {cfg.description}", "n_qubits": 1024, "vertices": 2048, "edges": 3072,
+                   "restarts_per_gpu": B, "segments": obj.dp_energy.plan.n_segments,
+                   "chi_max": obj.dp_energy.plan.chi_max, "l2": "flushed between timed steps (256 MiB memset, untimed)",
+                   "parallelism": "restarts as the batch dimension"},
+        "roofline": {"bound": "fp32_simt", "kernel": kname, "achieved": achieved, "peak": ffma.value,
+                     "unit": "TFLOP/s", "frac": achieved / ffma.value, "traffic": None,
+                     "peak_source": "measured FFMA probe (tq_ffma_peak) on this GPU in this run",
+                     "kernel_ms": {k: statistics.mean(vv) for k, vv in kt.items()}},
+        "hbm": {"achieved_gbs": byts / (ms * 1e-3) / 1e9, "peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
+                "frac": byts / (ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), "bytes_per_step": byts},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": circuit.n_params * 4,
+                "d2h_bytes_per_step": circuit.n_params * 4 + 8, "note": "single restart through mbe_objective"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--segments", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -392,6 +565,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.config == "cfg3":
+        run_cfg3(args, cfg)
     else:
         run_ours(args, cfg)
 

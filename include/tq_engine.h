@@ -63,9 +63,11 @@ typedef struct {
   double init[4];           /* input product-state vector of this qubit (re,im,re,im) */
 } tq_site;
 
-/* One operator of a column: selects table entry mat + digit (chain.py OP_DTYPE). */
+/* One operator of a column: selects table entry mat + digit (chain.py OP_DTYPE).
+ * toff: digit bits introduced by earlier ops of the column (digit-tree level width),
+ * tbase: entries held by the earlier levels of the column's digit tree. */
 typedef struct {
-  int32_t mat, lmat, src, shift, bits, tidx, gidx, pad;
+  int32_t mat, lmat, src, shift, bits, tidx, gidx, toff, tbase, pad;
 } tq_op;
 
 /* 2x2 factor table entry (chain.py MAT_DTYPE): kind 0 const, 1 rx, 2 ry, 3 rz. */
@@ -94,7 +96,7 @@ typedef struct {
 typedef struct {
   int32_t n_segments, n_sites, n_params, n_terms;
   int32_t chi_max, d_max, max_ops, max_lmat, max_train, n_gslots;
-  int32_t max_edges, pad0;
+  int32_t max_edges, max_tree; /* max_tree: largest digit tree (entries) of any column */
   int64_t env_total; /* complex elements of stored envs per theta-set */
   double e_const_re, e_const_im; /* identity-term coefficients */
   const tq_site* sites;

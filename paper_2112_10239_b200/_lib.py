@@ -32,7 +32,7 @@ class TqChain(ctypes.Structure):
         ("n_segments", ctypes.c_int32), ("n_sites", ctypes.c_int32), ("n_params", ctypes.c_int32),
         ("n_terms", ctypes.c_int32), ("chi_max", ctypes.c_int32), ("d_max", ctypes.c_int32),
         ("max_ops", ctypes.c_int32), ("max_lmat", ctypes.c_int32), ("max_train", ctypes.c_int32),
-        ("n_gslots", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("pad0", ctypes.c_int32),
+        ("n_gslots", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("max_tree", ctypes.c_int32),
         ("env_total", ctypes.c_int64),
         ("e_const_re", ctypes.c_double), ("e_const_im", ctypes.c_double),
         ("sites", ctypes.c_void_p), ("ops", ctypes.c_void_p), ("mats", ctypes.c_void_p),
@@ -148,6 +148,7 @@ class DevicePlan:
         ch.max_train = plan.max_train
         ch.n_gslots = plan.n_gslots
         ch.max_edges = plan.max_edges
+        ch.max_tree = plan.max_tree
         ch.env_total = plan.env_total
         ch.e_const_re = plan.e_const.real
         ch.e_const_im = plan.e_const.imag

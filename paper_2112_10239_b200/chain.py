@@ -48,7 +48,8 @@ SITE_DTYPE = np.dtype([
     ("init", "<f8", (4,)),
 ], align=True)
 OP_DTYPE = np.dtype([("mat", "<i4"), ("lmat", "<i4"), ("src", "<i4"), ("shift", "<i4"), ("bits", "<i4"),
-                     ("tidx", "<i4"), ("gidx", "<i4"), ("pad", "<i4")], align=True)
+                     ("tidx", "<i4"), ("gidx", "<i4"), ("toff", "<i4"), ("tbase", "<i4"), ("pad", "<i4")],
+                    align=True)
 MAT_DTYPE = np.dtype([("kind", "<i4"), ("slot", "<i4"), ("cls", "<i4"), ("pad", "<i4"),
                       ("angle", "<f8"), ("pscale", "<f8"), ("m", "<f8", (8,))], align=True)
 EDGE_DTYPE = np.dtype([("a", "<i4"), ("b", "<i4"), ("op", "<i4"), ("coef", "<i4")], align=True)
@@ -287,6 +288,7 @@ class ChainPlan:
     chi_max: int
     d_max: int
     max_edges: int
+    max_tree: int
     max_ops: int
     max_lmat: int
     max_train: int
@@ -346,7 +348,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
     sites, ops, mats, edges, fins, passes, segs = [], [], [], [], [], [], []
     mat_index = {}
     gred = {}  # theta slot -> list of absolute partial indices
-    chi_max, d_max, max_ops, max_lmat, max_train = 1, 1, 0, 1, 0
+    chi_max, d_max, max_ops, max_lmat, max_train, max_tree = 1, 1, 0, 1, 0, 1
     env_total = 0
     gslot_total = 0
     init_vecs = None if init is None else np.asarray(init, dtype=complex).reshape(n, 2)
@@ -423,6 +425,8 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
             rec["ent_begin"] = len(mats)
             lmat = 0
             ntrain = 0
+            toff = 0      # digit bits introduced before this op (digit-tree level index width)
+            tbase = 0     # entries of all previous tree levels
             for (src, shift, bits, specs) in col[q]:
                 o = np.zeros((), dtype=OP_DTYPE)
                 base = mat_block(specs)
@@ -438,8 +442,12 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
                     g_local += 1
                 else:
                     o["tidx"], o["gidx"] = -1, -1
+                o["toff"], o["tbase"] = toff, tbase
+                tbase += 1 << (toff + bits)
+                toff += bits
                 lmat += 1 << bits
                 ops.append(o)
+            max_tree = max(max_tree, tbase)
             rec["op_count"] = len(col[q])
             rec["lmat_count"] = lmat
             rec["n_train"] = ntrain
@@ -493,7 +501,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         sites=arr(sites, SITE_DTYPE), ops=arr(ops, OP_DTYPE), mats=arr(mats, MAT_DTYPE),
         edges=arr(edges, EDGE_DTYPE), fins=arr(fins, EDGE_DTYPE), passes=arr(passes, PASS_DTYPE),
         segs=arr(segs, SEG_DTYPE), gred_ptr=ptr, gred_idx=np.array(idx, dtype=np.int32),
-        chi_max=chi_max, d_max=d_max, max_edges=_max_edges(sites), max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
+        chi_max=chi_max, d_max=d_max, max_edges=_max_edges(sites), max_tree=max_tree, max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
         n_gslots=gslot_total, env_total=env_total, e_const=e_const, term_active=active,
     )
     plan.info = {"segments": len(segs), "sub_chain_sites": int(sum(int(s["site_count"]) for s in segs)),

@@ -49,16 +49,20 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
 
 // ------------------------------------------------------------------ kernel parameters
 struct Layout {          // byte offsets inside one team's shared-memory slab (host computed)
-  int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, sedge;
+  int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, obase, sedge;
+  int32_t tree;          // 0: per-pair column walks; 1: digit tree, dedicated levels; 2: digit tree in M/BR scratch
+  int32_t lev, ubuf;     // digit-tree level storage and the adjoint's ping-pong buffers
   int32_t team_bytes;
 };
 
 // Site edge staged in shared memory with its coefficient already resolved for this theta-set.
 template <typename R> struct SEdge { int a, b, op; R coef; };
 
-// Packed column op: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24]
+// Packed column op: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24] toff[24:29]
 __device__ __forceinline__ int oc_lmat(int c) { return c & 511; }
 __device__ __forceinline__ int oc_tidx(int c) { return ((c >> 18) & 63) - 1; }
+__device__ __forceinline__ int oc_toff(int c) { return (c >> 24) & 31; }
+__device__ __forceinline__ int oc_bits(int c) { return (c >> 16) & 3; }
 __device__ __forceinline__ int oc_digit(int c, int al, int be) {
   const int src = (c >> 9) & 3, shift = (c >> 11) & 31, mask = (1 << ((c >> 16) & 3)) - 1;
   return src == 0 ? 0 : (((src == 1 ? al : be) >> shift) & mask);
@@ -77,6 +81,18 @@ struct Params {
   int32_t store_env;
   int32_t mode;     // 0 energy-grad, 1 values
 };
+
+// Optional per-stage cycle accounting (diagnostic build with -DTQ_STAGE_TIMING only).
+#ifdef TQ_STAGE_TIMING
+__device__ unsigned long long g_stage_cycles[2][16];
+#define STAGE_BEGIN() long long _t_prev = clock64(); long long _acc[16]; for (int _i = 0; _i < 16; ++_i) _acc[_i] = 0;
+#define STAGE(k) do { const long long _t = clock64(); _acc[k] += _t - _t_prev; _t_prev = _t; } while (0)
+#define STAGE_END(kern) do { if (tid == 0) for (int _i = 0; _i < 16; ++_i) atomicAdd(&g_stage_cycles[kern][_i], (unsigned long long)_acc[_i]); } while (0)
+#else
+#define STAGE_BEGIN()
+#define STAGE(k)
+#define STAGE_END(kern)
+#endif
 
 // Team barrier: a warp team syncs with __syncwarp, a CTA team with __syncthreads.
 template <int TEAM> __device__ __forceinline__ void team_sync() {
@@ -98,7 +114,8 @@ template <typename C> __device__ __forceinline__ C pauli_fac(int op, int sp) {
 // the MPO edges of the current sweep with their coefficients looked up once.
 template <typename R, int TEAM>
 __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef_row, const tq_site& st, int tid, bool rl,
-                           typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, SEdge<R>* sedge) {
+                           typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
+                           SEdge<R>* sedge) {
   using C = typename CT<R>::T;
   for (int e = tid; e < st.lmat_count; e += TEAM) {
     const tq_mat& mt = ch.mats[st.ent_begin + e];
@@ -123,8 +140,9 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
   }
   for (int o = tid; o < st.op_count; o += TEAM) {
     const tq_op& op = ch.ops[st.op_begin + o];
-    ocode[o] = op.lmat | (op.src << 9) | (op.shift << 11) | (op.bits << 16) | ((op.tidx + 1) << 18);
+    ocode[o] = op.lmat | (op.src << 9) | (op.shift << 11) | (op.bits << 16) | ((op.tidx + 1) << 18) | (op.toff << 24);
     ogidx[o] = op.gidx;
+    obase[o] = op.tbase;
   }
   const int eb = rl ? st.rl_edge_begin : st.lr_edge_begin;
   const int ec = rl ? st.rl_edge_count : st.lr_edge_count;
@@ -167,6 +185,151 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
     A[al * LD + be] = v0; A[LD * LD + al * LD + be] = v1;   // A slots are LD*LD apart
     AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1);
   }
+}
+
+
+// ------------------------------------------------------------------ digit-tree column fold
+// The column's ops introduce bond digits one at a time, so after op l the distinct column
+// vectors are indexed by the digits introduced so far (toff_l + bits_l bits, the newest
+// digit on top).  Level l of the tree holds 2^(toff_l+bits_l) 2-vectors at lev[tbase_l];
+// the last level holds A[.][alpha][beta] at index idx(alpha, beta).  Cost per site is
+// sum_l 2^(bits so far) matvecs instead of chi_l*chi_r*L for per-pair walks.
+template <typename R, int TEAM>
+__device__ void tree_forward(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
+                             const int* obase, typename CT<R>::T* lev) {
+  using C = typename CT<R>::T;
+  const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+  for (int oi = 0; oi < st.op_count; ++oi) {
+    const int c = ocode[oi];
+    const int toff = oc_toff(c), nn = 1 << (toff + oc_bits(c));
+    const int base = obase[oi], pbase = oi ? obase[oi - 1] : 0;
+    const C* Mb = mres + 4 * oc_lmat(c);
+    for (int e = tid; e < nn; e += TEAM) {
+      const int idx = e & ((1 << toff) - 1);
+      const C* M = Mb + 4 * (e >> toff);
+      const C v0 = oi ? lev[2 * (pbase + idx)] : i0;
+      const C v1 = oi ? lev[2 * (pbase + idx) + 1] : i1;
+      C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
+      C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
+      lev[2 * (base + e)] = n0; lev[2 * (base + e) + 1] = n1;
+    }
+    team_sync<TEAM>();
+  }
+}
+
+__device__ __forceinline__ int tree_index(const int* ocode, int nops, int al, int be) {
+  int idx = 0;
+  for (int oi = 0; oi < nops; ++oi) {
+    const int c = ocode[oi];
+    if (oc_bits(c)) idx |= oc_digit(c, al, be) << oc_toff(c);
+  }
+  return idx;
+}
+
+// A[s] / AH[s] from the last tree level (zero where passthrough digits disagree).
+template <typename R, int LD, int TEAM>
+__device__ void tree_scatter(const tq_chain& ch, const tq_site& st, int tid, const int* ocode, const int* obase,
+                             const typename CT<R>::T* lev, typename CT<R>::T* A, typename CT<R>::T* AH, int lcr) {
+  using C = typename CT<R>::T;
+  const int npair = st.chi_l * st.chi_r;
+  const int last = st.op_count - 1;
+  const int lbase = last >= 0 ? obase[last] : 0;
+  for (int pi = tid; pi < npair; pi += TEAM) {
+    const int al = pi >> lcr, be = pi & (st.chi_r - 1);
+    C v0, v1;
+    if (st.pass_count && !pass_ok(ch, st, al, be)) { v0 = cmk<C>(R(0), R(0)); v1 = v0; }
+    else if (last < 0) { v0 = cmk<C>(R(st.init[0]), R(st.init[1])); v1 = cmk<C>(R(st.init[2]), R(st.init[3])); }
+    else {
+      const int idx = tree_index(ocode, st.op_count, al, be);
+      v0 = lev[2 * (lbase + idx)]; v1 = lev[2 * (lbase + idx) + 1];
+    }
+    A[al * LD + be] = v0; A[LD * LD + al * LD + be] = v1;
+    AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1);
+  }
+}
+
+// Column adjoint on the digit tree: U_last[idx] = sum over passthrough-matched (alpha, beta)
+// of (G[0], G[1])[alpha][beta]; walking down, every trainable rotation accumulates
+// Im<U_l, sigma V_l> and U_{l-1}[idx] = sum_d M_l(d)^H U_l[idx | d << toff_l].
+template <typename R, int LD, int TEAM>
+__device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                             const int* minfo, const int* ocode, const int* obase, const typename CT<R>::T* lev,
+                             typename CT<R>::T* ubuf, const typename CT<R>::T* G, R* contrib) {
+  using C = typename CT<R>::T;
+  constexpr int MS = LD * LD;
+  const int nops = st.op_count;
+  if (nops == 0) return;
+  const int clast = ocode[nops - 1];
+  const int nlast = 1 << (oc_toff(clast) + oc_bits(clast));
+  C* ua = ubuf;
+  C* ub = ubuf + 2 * nlast;
+  int npb = 0;
+  for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
+  for (int e = tid; e < nlast; e += TEAM) {
+    int al = 0, be = 0;
+    for (int oi = 0; oi < nops; ++oi) {
+      const int c = ocode[oi];
+      const int bits = oc_bits(c);
+      if (!bits) continue;
+      const int d = (e >> oc_toff(c)) & ((1 << bits) - 1);
+      const int src = (c >> 9) & 3, shift = (c >> 11) & 31;
+      if (src == 1) al |= d << shift; else be |= d << shift;
+    }
+    C g0 = cmk<C>(R(0), R(0)), g1 = g0;
+    for (int cmb = 0; cmb < (1 << npb); ++cmb) {
+      int a2 = al, b2 = be, used = 0;
+      for (int i = 0; i < st.pass_count; ++i) {
+        const tq_pass ps = ch.passes[st.pass_begin + i];
+        const int v = (cmb >> used) & ((1 << ps.bits) - 1);
+        a2 |= v << ps.sa; b2 |= v << ps.sb; used += ps.bits;
+      }
+      const C x0 = G[a2 * LD + b2], x1 = G[MS + a2 * LD + b2];
+      g0.x += x0.x; g0.y += x0.y; g1.x += x1.x; g1.y += x1.y;
+    }
+    ua[2 * e] = g0; ua[2 * e + 1] = g1;
+  }
+  for (int oi = nops - 1; oi >= 0; --oi) {
+    team_sync<TEAM>();
+    const int c = ocode[oi];
+    const int toff = oc_toff(c), bits = oc_bits(c);
+    const int nn = 1 << (toff + bits);
+    const int tix = oc_tidx(c);
+    const C* V = lev + 2 * obase[oi];
+    const int lm = oc_lmat(c);
+    if (tix >= 0) {
+      R acc = R(0);
+      for (int e = tid; e < nn; e += TEAM) {
+        const int ent = lm + (e >> toff);
+        const int kind = minfo[ent] & 0xff;
+        if (kind == 0) continue;
+        const C u0 = ua[2 * e], u1 = ua[2 * e + 1];
+        const C v0 = V[2 * e], v1 = V[2 * e + 1];
+        C s0, s1;
+        if (kind == 1) { s0 = v1; s1 = v0; }
+        else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
+        else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
+        C d = cmk<C>(R(0), R(0));
+        cfmac(d, u0, s0); cfmac(d, u1, s1);
+        acc += d.y;
+      }
+      contrib[tix * TEAM + tid] += acc;
+    }
+    if (oi > 0) {
+      const int np = 1 << toff;
+      for (int idx = tid; idx < np; idx += TEAM) {
+        C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+        for (int d = 0; d < (1 << bits); ++d) {
+          const C* M = mres + 4 * (lm + d);
+          const C u0 = ua[2 * (idx | (d << toff))], u1 = ua[2 * (idx | (d << toff)) + 1];
+          cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
+          cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
+        }
+        ub[2 * idx] = w0; ub[2 * idx + 1] = w1;
+      }
+      C* t = ua; ua = ub; ub = t;
+    }
+  }
+  team_sync<TEAM>();
 }
 
 // Register-tiled complex GEMM over a group of equally shaped tasks:
@@ -215,7 +378,8 @@ struct TeamSmem {
   using C = typename CT<R>::T;
   C *A, *AH, *ENV, *M, *BR, *PIN, *MR, *mres;
   R *contrib, *mps;
-  int *minfo, *ocode, *ogidx;
+  int *minfo, *ocode, *ogidx, *obase;
+  C *lev, *ubuf;
   SEdge<R>* sedge;
   __device__ TeamSmem(unsigned char* base, const Layout& L) {
     A = reinterpret_cast<C*>(base + L.a); AH = reinterpret_cast<C*>(base + L.ah);
@@ -225,6 +389,8 @@ struct TeamSmem {
     contrib = reinterpret_cast<R*>(base + L.contrib); mps = reinterpret_cast<R*>(base + L.mps);
     minfo = reinterpret_cast<int*>(base + L.minfo); ocode = reinterpret_cast<int*>(base + L.ocode);
     ogidx = reinterpret_cast<int*>(base + L.ogidx); sedge = reinterpret_cast<SEdge<R>*>(base + L.sedge);
+    obase = reinterpret_cast<int*>(base + L.obase);
+    lev = reinterpret_cast<C*>(base + L.lev); ubuf = reinterpret_cast<C*>(base + L.ubuf);
   }
 };
 
@@ -236,26 +402,157 @@ __device__ __forceinline__ void bracket_stage(int tid, int ntarget, int ec, cons
                                               int lcl, int lcr) {
   using C = typename CT<R>::T;
   constexpr int MS = LD * LD;
+  constexpr int U = 4;   // independent elements per thread iteration (ILP)
   const int lpair = lcl + lcr;
   const int nel = (ntarget * 2) << lpair;
-  for (int e = tid; e < nel; e += TEAM) {
-    const int ij = e & ((1 << lpair) - 1);
-    const int ts = e >> lpair;
-    const int t = ts >> 1, sp = ts & 1;
-    const int off = (ij >> lcr) * LD + (ij & ((1 << lcr) - 1));
-    R ax = R(0), ay = R(0);
+  for (int e0 = tid; e0 < nel; e0 += TEAM * U) {
+    int off[U], t[U], sp[U];
+    bool on[U];
+    R ax[U], ay[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * TEAM;
+      on[u] = e < nel;
+      const int ij = e & ((1 << lpair) - 1);
+      const int ts = e >> lpair;
+      t[u] = ts >> 1; sp[u] = ts & 1;
+      off[u] = (ij >> lcr) * LD + (ij & ((1 << lcr) - 1));
+      ax[u] = R(0); ay[u] = R(0);
+    }
     for (int ei = 0; ei < ec; ++ei) {
       const SEdge<R> ed = sedge[ei];
-      if ((rl ? ed.a : ed.b) != t) continue;
-      const int src = rl ? ed.b : ed.a;
-      const int s = pauli_src<C>(ed.op, sp);
-      const C f = pauli_fac<C>(ed.op, sp);
-      const C nv = SRC[(src * 2 + s) * MS + off];
-      const C tt = cmul(f, nv);
-      ax = fma(ed.coef, tt.x, ax);
-      ay = fma(ed.coef, tt.y, ay);
+      const int tgt = rl ? ed.a : ed.b, src = rl ? ed.b : ed.a;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!on[u] || tgt != t[u]) continue;
+        const int s = pauli_src<C>(ed.op, sp[u]);
+        const C f = pauli_fac<C>(ed.op, sp[u]);
+        const C tt = cmul(f, SRC[(src * 2 + s) * MS + off[u]]);
+        ax[u] = fma(ed.coef, tt.x, ax[u]);
+        ay[u] = fma(ed.coef, tt.y, ay[u]);
+      }
     }
-    BR[ts * MS + off] = cmk<C>(ax, ay);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (on[u]) BR[(t[u] * 2 + sp[u]) * MS + off[u]] = cmk<C>(ax[u], ay[u]);
+  }
+}
+
+// Rows per item for the fused product+bracket stages: enough items for every thread.
+__device__ __forceinline__ int fused_rows(int m, int nel, int team, int rtmax) {
+  int rt = nel / team;
+  rt = rt >= 4 ? 4 : (rt >= 2 ? 2 : 1);
+  if (rt > rtmax) rt = rtmax;
+  if (rt > m) rt = m;
+  return rt;
+}
+
+// Select acc[idx][s][r] with runtime idx/s from a register array (unrolled, no local memory).
+template <typename C, int DM, int RT>
+__device__ __forceinline__ C pick(const C (&acc)[DM][2][RT], int idx, int s, int r) {
+  C v = acc[0][0][0];
+#pragma unroll
+  for (int x = 0; x < DM; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int z = 0; z < RT; ++z)
+        if (x == idx && y == s && z == r) v = acc[x][y][z];
+  return v;
+}
+
+// Fused MPO product + bracket.  Right-to-left form (rl = true):
+//   N[b][s] = A[s] (m x n) * P[b] (n x n);  BR[a][s'] = sum_edges(a<-b) coef <s'|O|s> N[b][s]
+// Left-to-right form (rl = false):
+//   M[a][s] = Lam[a] (m x m) * A[s] (m x n);  BR[b][s'] = sum_edges(a->b) coef <s'|O|s> M[a][s]
+// Every item owns rows i0..i0+rt-1 of one column j for ALL (channel, s) products, so the
+// products stay in registers and the bracket combination never touches shared memory.
+template <typename R, int LD, int TEAM, int DM, int RT>
+__device__ void product_bracket(int tid, bool rl, int nsrc, int ntgt, int m, int n, int lm, int ln,
+                                const typename CT<R>::T* A, const typename CT<R>::T* ENV,
+                                const SEdge<R>* sedge, int ec, typename CT<R>::T* BR) {
+  using C = typename CT<R>::T;
+  constexpr int MS = LD * LD;
+  const int rt = fused_rows(m, m * n, TEAM, RT);
+  const int lrt = rt == 4 ? 2 : (rt == 2 ? 1 : 0);
+  const int items = (m >> lrt) << ln;
+  const int kk = rl ? n : m;
+  for (int it = tid; it < items; it += TEAM) {
+    const int j = it & (n - 1);
+    const int i0 = (it >> ln) << lrt;
+    C acc[DM][2][RT];
+#pragma unroll
+    for (int x = 0; x < DM; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int z = 0; z < RT; ++z) acc[x][y][z] = cmk<C>(R(0), R(0));
+    if (rl) {
+      for (int k = 0; k < kk; ++k) {
+        C pb[DM];
+#pragma unroll
+        for (int x = 0; x < DM; ++x) pb[x] = x < nsrc ? ENV[x * MS + k * LD + j] : cmk<C>(R(0), R(0));
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int z = 0; z < RT; ++z) {
+            if (z < rt) {
+              const C a = A[y * MS + (i0 + z) * LD + k];
+#pragma unroll
+              for (int x = 0; x < DM; ++x) if (x < nsrc) cfma(acc[x][y][z], a, pb[x]);
+            }
+          }
+      }
+    } else {
+      for (int k = 0; k < kk; ++k) {
+        const C b0 = A[k * LD + j], b1 = A[MS + k * LD + j];
+#pragma unroll
+        for (int x = 0; x < DM; ++x) {
+          if (x < nsrc) {
+#pragma unroll
+            for (int z = 0; z < RT; ++z) {
+              if (z < rt) {
+                const C l = ENV[x * MS + (i0 + z) * LD + k];
+                cfma(acc[x][0][z], l, b0);
+                cfma(acc[x][1][z], l, b1);
+              }
+            }
+          }
+        }
+      }
+    }
+    C br[DM][2][RT];
+#pragma unroll
+    for (int x = 0; x < DM; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int z = 0; z < RT; ++z) br[x][y][z] = cmk<C>(R(0), R(0));
+    for (int ei = 0; ei < ec; ++ei) {
+      const SEdge<R> ed = sedge[ei];
+      const int src = rl ? ed.b : ed.a, tgt = rl ? ed.a : ed.b;
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp) {
+        const int s = pauli_src<C>(ed.op, sp);
+        C f = pauli_fac<C>(ed.op, sp);
+        f.x *= ed.coef; f.y *= ed.coef;
+#pragma unroll
+        for (int z = 0; z < RT; ++z) {
+          const C v = cmul(f, pick<C, DM, RT>(acc, src, s, z));
+#pragma unroll
+          for (int x = 0; x < DM; ++x)
+            if (x == tgt) { br[x][sp][z].x += v.x; br[x][sp][z].y += v.y; }
+        }
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < DM; ++x)
+      if (x < ntgt)
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int z = 0; z < RT; ++z)
+            if (z < rt) BR[(x * 2 + y) * MS + (i0 + z) * LD + j] = br[x][y][z];
   }
 }
 
@@ -276,6 +573,9 @@ rl_sweep(Params p) {
   constexpr int LD = CHI + 1;
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
+  constexpr bool FUSE = false;                    // register-fused product+bracket (measured slower; kept for study)
+  constexpr int FDM = 4;                          // channels handled by the fused stages
+  constexpr int FRT = sizeof(R) == 4 ? 4 : 2;     // max rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -288,6 +588,7 @@ rl_sweep(Params p) {
   const R* coef_b = p.coef ? reinterpret_cast<const R*>(p.coef) + (int64_t)b * p.coef_stride : nullptr;
   C* PIN = sm.ENV;   // P at the right cut (in) / left cut (out)
   C* N = sm.M;
+  STAGE_BEGIN();
 
   const tq_segment seg = p.c.segs[g];
   C* env_g = reinterpret_cast<C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
@@ -301,18 +602,30 @@ rl_sweep(Params p) {
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
-    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, true, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.sedge);
+    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, true, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     team_sync<TEAM>();
+    STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
     team_sync<TEAM>();
-    // N[b][s] = A[s] * P[b]
-    gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-        [&](int t, int) { return sm.A + (t & 1) * MS; },
-        [&](int t, int) { return PIN + (t >> 1) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
-    team_sync<TEAM>();
-    bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
-    team_sync<TEAM>();
+    STAGE(1);
+    if (FUSE && db <= FDM && da <= FDM) {
+      // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, sm.sedge,
+                                              st.rl_edge_count, sm.BR);
+      team_sync<TEAM>();
+      STAGE(2);
+    } else {
+      // N[b][s] = A[s] * P[b]
+      gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+          [&](int t, int) { return sm.A + (t & 1) * MS; },
+          [&](int t, int) { return PIN + (t >> 1) * MS; },
+          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+      team_sync<TEAM>();
+      STAGE(2);
+      bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
+      team_sync<TEAM>();
+      STAGE(3);
+    }
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     const bool store = p.store_env && st.env_out >= 0;
     C* envo = env_g + (store ? st.env_out : 0);
@@ -327,8 +640,10 @@ rl_sweep(Params p) {
           }
         });
     team_sync<TEAM>();
+    STAGE(4);
   }
   if (tid == 0) reinterpret_cast<C*>(p.epart)[(size_t)b * S + g] = PIN[0];
+  STAGE_END(0);
 }
 
 // ------------------------------------------------------------------ left-to-right sweep
@@ -341,6 +656,9 @@ lr_sweep(Params p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
+  constexpr bool FUSE = false;                    // register-fused product+bracket (measured slower; kept for study)
+  constexpr int FDM = 4;                          // channels handled by the fused stages
+  constexpr int FRT = sizeof(R) == 4 ? 4 : 2;     // max rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -355,6 +673,7 @@ lr_sweep(Params p) {
   C* M = sm.M;
   C* G = sm.M;  // gradient cores alias the M slots (dead after the bracket stage)
   C* PIN = sm.PIN;
+  STAGE_BEGIN();
 
   const tq_segment seg = p.c.segs[g];
   const C* env_g = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
@@ -366,7 +685,7 @@ lr_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = p.mode == 0 ? st.rl_db : 1;
-    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, false, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.sedge);
+    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, false, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
@@ -377,16 +696,28 @@ lr_sweep(Params p) {
       }
     }
     team_sync<TEAM>();
+    STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
     team_sync<TEAM>();
-    // M[a][s] = Lam[a] * A[s]
-    gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cl, 1,
-        [&](int t, int) { return LAM + (t >> 1) * MS; },
-        [&](int t, int) { return sm.A + (t & 1) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
-    team_sync<TEAM>();
-    bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
-    team_sync<TEAM>();
+    STAGE(1);
+    if (FUSE && p.mode == 0 && da <= FDM && db <= FDM) {
+      // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, sm.A, LAM, sm.sedge,
+                                              st.lr_edge_count, sm.BR);
+      team_sync<TEAM>();
+      STAGE(2);
+    } else {
+      // M[a][s] = Lam[a] * A[s]
+      gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cl, 1,
+          [&](int t, int) { return LAM + (t >> 1) * MS; },
+          [&](int t, int) { return sm.A + (t & 1) * MS; },
+          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+      team_sync<TEAM>();
+      STAGE(2);
+      bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
+      team_sync<TEAM>();
+      STAGE(3);
+    }
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
     gemm_group<C, LD, TEAM>(tid, db, cr, cr, cl, 2,
         [&](int, int qq) { return sm.AH + qq * MS; },
@@ -399,13 +730,18 @@ lr_sweep(Params p) {
           [&](int, int qq) { return PIN + qq * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
+      STAGE(4);
       // ---- column adjoint: per (alpha, beta) pair forward fold keeping the components
       // projectors discard, then the backward walk accumulating Im<u, sigma v>.
       const int ntr = st.n_train;
       R* contrib = sm.contrib;
       for (int t = 0; t < ntr; ++t) contrib[t * TEAM + tid] = R(0);
-      const int npair = cl * cr;
+      const int npair = p.L.tree ? 0 : cl * cr;
       const int nops = st.op_count;
+      if (p.L.tree) {
+        tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
+        tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
+      }
       for (int pi = tid; pi < npair; pi += TEAM) {
         const int al = pi >> lcr, be = pi & (cr - 1);
         if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
@@ -464,6 +800,7 @@ lr_sweep(Params p) {
         }
       }
       team_sync<TEAM>();
+      STAGE(5);
       // deterministic per-op reduction: warp w handles ops w, w + nwarps, ...
       {
         const int warp = tid >> 5, lane = tid & 31;
@@ -479,6 +816,7 @@ lr_sweep(Params p) {
         }
       }
       team_sync<TEAM>();
+      STAGE(6);
     } else {
       // ---- values: rho_a[s'][s] = <A[s'], M[a][s] R> for every source channel a
       gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cr, 1,
@@ -486,6 +824,7 @@ lr_sweep(Params p) {
           [&](int, int) { return PIN; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(sm.MR + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
+      STAGE(7);
       if (st.fin_count > 0) {
         const int ncombo = da * 4;  // (a, s', s)
         R* part = sm.contrib;       // [2 * ncombo][TEAM] partial sums (re, im)
@@ -500,6 +839,7 @@ lr_sweep(Params p) {
           part[(2 * cmb + 1) * TEAM + tid] = acc.y;
         }
         team_sync<TEAM>();
+        STAGE(8);
         if (tid < 32) {  // reduce and finalise (one warp, fixed order)
           for (int fi = 0; fi < st.fin_count; ++fi) {
             const tq_edge fe = p.c.fins[st.fin_begin + fi];
@@ -526,8 +866,10 @@ lr_sweep(Params p) {
         }
       }
       team_sync<TEAM>();
+      STAGE(9);
     }
   }
+  STAGE_END(1);
 }
 
 
@@ -541,7 +883,7 @@ struct InnerParams {
   const void* theta_bra; int64_t bra_stride;
   double* out;
   int32_t team_bytes;
-  int32_t off_ak, off_ahk, off_ab, off_ahb, off_t, off_l, off_mk, off_ik, off_pk, off_ok, off_gk, off_mb, off_ib, off_pb, off_ob, off_gb;
+  int32_t off_ak, off_ahk, off_ab, off_ahb, off_t, off_l, off_mk, off_ik, off_pk, off_ok, off_gk, off_qk, off_mb, off_ib, off_pb, off_ob, off_gb, off_qb;
 };
 
 template <typename R, int CHI, int TEAM>
@@ -569,10 +911,12 @@ inner_sweep(InnerParams p) {
     const tq_site sb = p.bra.sites[p.bra.segs[0].site_begin + q];
     stage_site<R, TEAM>(p.ket, thk, nullptr, sk, tid, true, reinterpret_cast<C*>(base + p.off_mk),
                         reinterpret_cast<int*>(base + p.off_ik), reinterpret_cast<R*>(base + p.off_pk),
-                        reinterpret_cast<int*>(base + p.off_ok), reinterpret_cast<int*>(base + p.off_gk), nullptr);
+                        reinterpret_cast<int*>(base + p.off_ok), reinterpret_cast<int*>(base + p.off_gk),
+                        reinterpret_cast<int*>(base + p.off_qk), nullptr);
     stage_site<R, TEAM>(p.bra, thb, nullptr, sb, tid, true, reinterpret_cast<C*>(base + p.off_mb),
                         reinterpret_cast<int*>(base + p.off_ib), reinterpret_cast<R*>(base + p.off_pb),
-                        reinterpret_cast<int*>(base + p.off_ob), reinterpret_cast<int*>(base + p.off_gb), nullptr);
+                        reinterpret_cast<int*>(base + p.off_ob), reinterpret_cast<int*>(base + p.off_gb),
+                        reinterpret_cast<int*>(base + p.off_qb), nullptr);
     team_sync<TEAM>();
     fold_site<R, LD, TEAM>(p.ket, sk, tid, reinterpret_cast<C*>(base + p.off_mk), reinterpret_cast<int*>(base + p.off_ok),
                            Ak, AHk, 31 - __clz(sk.chi_r));
@@ -649,7 +993,7 @@ static tq_status fail(tq_status s, const char* msg) {
   return s;
 }
 
-static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 256); }
+static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 512); }
 static int chi_bucket(int chi) { int c = 2; while (c < chi) c <<= 1; return c; }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -682,7 +1026,25 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.mps = (int32_t)off; off += align_up((size_t)c->max_lmat * rsz, 16);
   L.ocode = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.ogidx = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
+  L.obase = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.sedge = (int32_t)off; off += align_up((size_t)(c->max_edges > 0 ? c->max_edges : 1) * (rsz == 8 ? 24 : 16), 16);
+  // digit tree: levels (+ adjoint ping-pong buffers in the gradient sweep)
+  const size_t lev_bytes = align_up((size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz, 16);
+  const size_t u_bytes = (lr && mode == 0) ? (size_t)2 * chi * chi * 2 * csz : 0;
+  const size_t budget = (size_t)227 * 1024 / (team == 32 ? 4 : 1);
+  if (!lr || mode != 0 || chi < 16) {
+    L.tree = 0; L.lev = 0; L.ubuf = 0;   // per-pair walks (the tree's serial levels lose at small chi)
+  } else if (align_up(off + lev_bytes + u_bytes, 128) <= budget) {
+    L.tree = 1; L.lev = (int32_t)off; off += lev_bytes; L.ubuf = (int32_t)off; off += u_bytes;
+  } else {
+    // scratch in the M/BR slots: free during the fold; the gradient sweep rebuilds the levels
+    // for its adjoint after G (which occupies the first two M slots)
+    const size_t skip = (lr && mode == 0) ? 2 * ms : 0;
+    const size_t avail = (size_t)4 * D * ms - skip;
+    if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + skip); L.ubuf = (int32_t)(L.lev + lev_bytes); }
+    else { L.tree = 0; L.lev = 0; L.ubuf = 0; }
+  }
+  if (L.tree == 2 && L.contrib == L.br) { L.contrib = (int32_t)off; off += align_up(need, 16); }
   L.team_bytes = (int32_t)align_up(off, 128);
   return L;
 }
@@ -707,7 +1069,7 @@ static thread_local Timing g_timing = {{nullptr, nullptr, nullptr, nullptr}, fal
 
 template <typename R, int CHI>
 static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
-  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 256);
+  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   const int items = prm.batch * prm.c.n_segments;
   const int grid = (items + TEAMS - 1) / TEAMS;
@@ -813,7 +1175,7 @@ static tq_status values_impl(const tq_chain* c, int batch, const void* theta, in
 
 template <typename R, int CHI>
 static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
-  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 256);
+  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   const size_t csz = 2 * sizeof(R), ms = (size_t)(CHI + 1) * (CHI + 1) * csz;
   size_t off = 0;
@@ -823,9 +1185,11 @@ static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
   ip.off_mk = take((size_t)ip.ket.max_lmat * 4 * csz); ip.off_ik = take((size_t)ip.ket.max_lmat * 4);
   ip.off_pk = take((size_t)ip.ket.max_lmat * sizeof(R)); ip.off_ok = take((size_t)(ip.ket.max_ops + 1) * 4);
   ip.off_gk = take((size_t)(ip.ket.max_ops + 1) * 4);
+  ip.off_qk = take((size_t)(ip.ket.max_ops + 1) * 4);
   ip.off_mb = take((size_t)ip.bra.max_lmat * 4 * csz); ip.off_ib = take((size_t)ip.bra.max_lmat * 4);
   ip.off_pb = take((size_t)ip.bra.max_lmat * sizeof(R)); ip.off_ob = take((size_t)(ip.bra.max_ops + 1) * 4);
   ip.off_gb = take((size_t)(ip.bra.max_ops + 1) * 4);
+  ip.off_qb = take((size_t)(ip.bra.max_ops + 1) * 4);
   ip.team_bytes = (int32_t)align_up(off, 128);
   const size_t smem = (size_t)ip.team_bytes * TEAMS;
   if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "inner product layout exceeds shared memory");
@@ -961,6 +1325,15 @@ int32_t tq_abi_layout(int32_t* sizes, int32_t n) {
   for (int i = 0; i < n && i < 7; ++i) sizes[i] = v[i];
   return 7;
 }
+
+#ifdef TQ_STAGE_TIMING
+int32_t tq_stage_cycles(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, tq::g_stage_cycles, sizeof(unsigned long long) * 32);
+  unsigned long long z[32] = {0};
+  cudaMemcpyToSymbol(tq::g_stage_cycles, z, sizeof(z));
+  return 32;
+}
+#endif
 
 const char* tq_build_info(void) {
   return "tq_engine sm_100a: rl_sweep/lr_sweep<float|double, chi 2..32>, reduce_energy, reduce_grad, inner_sweep, ffma_probe";

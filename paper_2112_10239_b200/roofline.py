@@ -20,6 +20,8 @@ import numpy as np
 
 
 def sweep_cmacs(plan) -> dict:
+    """cMACs per theta-set: 'rl' right-to-left sweep, 'lr' left-to-right sweep (gradient
+    mode with the column adjoint, or values mode with the rho contractions)."""
     s = plan.sites
     cl = s["chi_l"].astype(np.float64)
     cr = s["chi_r"].astype(np.float64)
@@ -29,7 +31,12 @@ def sweep_cmacs(plan) -> dict:
     rl = 2 * s["rl_db"] * cl * cr * cr + 2 * s["rl_da"] * cl * cl * cr + 2 * s["rl_edge_count"] * cl * cr
     lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl + 2 * s["lr_db"] * cl * cr * cr
           + 2 * s["lr_edge_count"] * cl * cr)
-    adj = pairs * nops * 12
+    if plan.mode == "values":
+        lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl + 2 * s["lr_da"] * cl * cr * cr
+              + 4 * s["lr_da"] * cl * cr * (s["fin_count"] > 0) + 2 * s["lr_edge_count"] * cl * cr)
+        adj = np.zeros_like(fold)
+    else:
+        adj = pairs * nops * 12
     return {"rl": float(np.sum(fold + rl)), "lr": float(np.sum(fold + lr + adj)),
             "fold": float(np.sum(fold)), "adjoint": float(np.sum(adj))}
 

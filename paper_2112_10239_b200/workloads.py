@@ -67,6 +67,9 @@ CONFIGS = {
                    "TTCircuit 10 qubits, 4 layers RotY+CNOT, TFIM energy+gradient"),
     "cfg2": Config("cfg2", 100, 10, "ry", "cz", 256, True,
                    "TTCircuit 100 qubits, 10 layers RotY+CZ, TFIM energy+gradient, 256 parameter sets"),
+    "cfg3": Config("cfg3", 1024, 4, "ry+rz", "cz", 8, True,
+                   "MBE MaxCut, random 3-regular graph V=2048 (3072 edges), brickwork_ansatz(1024, 4), "
+                   "one Adam step (loss + gradient) per restart"),
     "cfg4": Config("cfg4", 1000, 20, "ry", "cz", 64, True,
                    "TTCircuit 1000 qubits, 20 layers RotY+CZ, TFIM energy+gradient"),
     "cfg5": Config("cfg5", 1024, 10, "ry", "cz", 64, False,
