@@ -231,12 +231,14 @@ def factored_chi(n, tgates) -> int:
 
 def resident_teams(chi: int, d: int = 3) -> int:
     """Work items resident per SM, from the kernels' shared-memory layout (lr sweep,
-    complex64): (4 + 6D) matrix slots of (chi+1)^2 complex plus descriptors.  Warp
-    teams (chi <= 8) come 4 per CTA; chi 16/32 teams are whole CTAs."""
+    complex64): 4 + 4D matrix slots of (chi+1)^2 complex for the fused small-chi path,
+    2 + 6D otherwise, plus descriptors.  Warp teams (chi <= 8) come 4 per CTA; chi 16/32
+    teams are whole CTAs."""
     b = 2
     while b < chi:
         b <<= 1
-    team_bytes = (4 + 6 * d) * (b + 1) ** 2 * 8 + 4096
+    slots = 4 + 4 * d if b <= 8 else 2 + 6 * d      # fused small-chi layout vs unfused (gradient sweep)
+    team_bytes = slots * (b + 1) ** 2 * 8 + 4096
     smem = 227 * 1024
     if b <= 8:
         ctas = max(1, smem // (4 * team_bytes))

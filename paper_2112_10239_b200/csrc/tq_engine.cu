@@ -47,6 +47,12 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
   acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
 }
 
+// acc += a * conj(b)
+template <typename C> __device__ __forceinline__ void cfmacb(C& acc, C a, C b) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y); acc.y = fma(-a.x, b.y, acc.y);
+}
+
 // ------------------------------------------------------------------ kernel parameters
 struct Layout {          // byte offsets inside one team's shared-memory slab (host computed)
   int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, obase, sedge;
@@ -141,7 +147,7 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
   for (int o = tid; o < st.op_count; o += TEAM) {
     const tq_op& op = ch.ops[st.op_begin + o];
     ocode[o] = op.lmat | (op.src << 9) | (op.shift << 11) | (op.bits << 16) | ((op.tidx + 1) << 18) | (op.toff << 24);
-    ogidx[o] = op.gidx;
+    if (op.tidx >= 0) ogidx[op.tidx] = op.gidx;   // trainable index -> partial-gradient slot
     obase[o] = op.tbase;
   }
   const int eb = rl ? st.rl_edge_begin : st.lr_edge_begin;
@@ -183,7 +189,7 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
       }
     }
     A[al * LD + be] = v0; A[LD * LD + al * LD + be] = v1;   // A slots are LD*LD apart
-    AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1);
+    if (AH) { AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1); }
   }
 }
 
@@ -244,7 +250,7 @@ __device__ void tree_scatter(const tq_chain& ch, const tq_site& st, int tid, con
       v0 = lev[2 * (lbase + idx)]; v1 = lev[2 * (lbase + idx) + 1];
     }
     A[al * LD + be] = v0; A[LD * LD + al * LD + be] = v1;
-    AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1);
+    if (AH) { AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1); }
   }
 }
 
@@ -336,8 +342,9 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
 //   C_t[m x n] = sum_{q < nq} A_{t,q}[m x kk] * B_{t,q}[kk x n]   (all row stride LD)
 // Each item computes rt consecutive rows of one column; a warp's lanes walk columns so the
 // A operand is a broadcast and the B operand a contiguous row.
-template <typename C, int LD, int TEAM, typename FA, typename FB, typename FS>
+template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, typename FA, typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
+  // CTA: the A operand is stored as X (kk x m) and used as X^H; CTB likewise for B (n x kk).
   const int rt = m >= 4 ? 4 : m;
   const int lrt = rt == 4 ? 2 : (rt == 2 ? 1 : 0);
   const int ln = 31 - __clz(n);
@@ -351,20 +358,35 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
     const int i0 = (r >> ln) << lrt;
     C acc0 = {0, 0}, acc1 = {0, 0}, acc2 = {0, 0}, acc3 = {0, 0};
     for (int q = 0; q < nq; ++q) {
-      const C* Ab = fa(task, q) + i0 * LD;
-      const C* Bb = fb(task, q) + j;
+      const C* Ab = fa(task, q) + (CTA ? i0 : i0 * LD);
+      const C* Bb = fb(task, q) + (CTB ? j * LD : j);
+      const int sa = CTA ? LD : 1;      // stride of A along k
+      const int ra = CTA ? 1 : LD;      // stride of A along rows
+      const int sb = CTB ? 1 : LD;      // stride of B along k
       if (rt == 4) {
 #pragma unroll 4
         for (int k = 0; k < kk; ++k) {
-          const C bv = Bb[k * LD];
-          cfma(acc0, Ab[k], bv); cfma(acc1, Ab[LD + k], bv);
-          cfma(acc2, Ab[2 * LD + k], bv); cfma(acc3, Ab[3 * LD + k], bv);
+          const C bv = Bb[k * sb];
+          const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
+          if (CTA) {
+            if (CTB) { C cb = cconj(bv); cfmac(acc0, a0, cb); cfmac(acc1, a1, cb); cfmac(acc2, a2, cb); cfmac(acc3, a3, cb); }
+            else { cfmac(acc0, a0, bv); cfmac(acc1, a1, bv); cfmac(acc2, a2, bv); cfmac(acc3, a3, bv); }
+          } else if (CTB) {
+            cfmacb(acc0, a0, bv); cfmacb(acc1, a1, bv); cfmacb(acc2, a2, bv); cfmacb(acc3, a3, bv);
+          } else {
+            cfma(acc0, a0, bv); cfma(acc1, a1, bv); cfma(acc2, a2, bv); cfma(acc3, a3, bv);
+          }
         }
       } else {
         for (int k = 0; k < kk; ++k) {
-          const C bv = Bb[k * LD];
-          cfma(acc0, Ab[k], bv);
-          if (rt == 2) cfma(acc1, Ab[LD + k], bv);
+          const C bv = Bb[k * sb];
+          const C a0 = Ab[k * sa];
+          const C b2 = CTB ? cconj(bv) : bv;
+          if (CTA) cfmac(acc0, a0, b2); else cfma(acc0, a0, b2);
+          if (rt == 2) {
+            const C a1 = Ab[ra + k * sa];
+            if (CTA) cfmac(acc1, a1, b2); else cfma(acc1, a1, b2);
+          }
         }
       }
     }
@@ -573,9 +595,9 @@ rl_sweep(Params p) {
   constexpr int LD = CHI + 1;
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
-  constexpr bool FUSE = false;                    // register-fused product+bracket (measured slower; kept for study)
+  constexpr bool FUSE = CHI <= 8;                 // register-fused product+bracket, one element per thread
   constexpr int FDM = 4;                          // channels handled by the fused stages
-  constexpr int FRT = sizeof(R) == 4 ? 4 : 2;     // max rows per fused item
+  constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -605,7 +627,7 @@ rl_sweep(Params p) {
     stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, true, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     team_sync<TEAM>();
     STAGE(0);
-    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
+    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     STAGE(1);
     if (FUSE && db <= FDM && da <= FDM) {
@@ -629,9 +651,9 @@ rl_sweep(Params p) {
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     const bool store = p.store_env && st.env_out >= 0;
     C* envo = env_g + (store ? st.env_out : 0);
-    gemm_group<C, LD, TEAM>(tid, da, cl, cl, cr, 2,
+    gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2,
         [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
-        [&](int, int qq) { return sm.AH + qq * MS; },
+        [&](int, int qq) { return sm.A + qq * MS; },
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
           store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
           if (store) {
@@ -656,9 +678,9 @@ lr_sweep(Params p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
-  constexpr bool FUSE = false;                    // register-fused product+bracket (measured slower; kept for study)
+  constexpr bool FUSE = CHI <= 8;                 // register-fused product+bracket, one element per thread
   constexpr int FDM = 4;                          // channels handled by the fused stages
-  constexpr int FRT = sizeof(R) == 4 ? 4 : 2;     // max rows per fused item
+  constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -697,7 +719,7 @@ lr_sweep(Params p) {
     }
     team_sync<TEAM>();
     STAGE(0);
-    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, sm.AH, lcr);
+    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     STAGE(1);
     if (FUSE && p.mode == 0 && da <= FDM && db <= FDM) {
@@ -719,8 +741,8 @@ lr_sweep(Params p) {
       STAGE(3);
     }
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
-    gemm_group<C, LD, TEAM>(tid, db, cr, cr, cl, 2,
-        [&](int, int qq) { return sm.AH + qq * MS; },
+    gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2,
+        [&](int, int qq) { return sm.A + qq * MS; },
         [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     if (p.mode == 0) {
@@ -737,6 +759,7 @@ lr_sweep(Params p) {
       R* contrib = sm.contrib;
       for (int t = 0; t < ntr; ++t) contrib[t * TEAM + tid] = R(0);
       const int npair = p.L.tree ? 0 : cl * cr;
+      const bool one_pair = npair <= TEAM;
       const int nops = st.op_count;
       if (p.L.tree) {
         tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
@@ -776,7 +799,8 @@ lr_sweep(Params p) {
             else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
             C d = cmk<C>(R(0), R(0));
             cfmac(d, u0, s0); cfmac(d, u1, s1);
-            contrib[tix * TEAM + tid] += d.y;
+            if (one_pair) contrib[tix * TEAM + tid] = d.y;
+            else contrib[tix * TEAM + tid] += d.y;
           }
           const C* Mm = sm.mres + 4 * e;
           C w0 = cmk<C>(R(0), R(0)), w1 = w0;   // u <- M^H u
@@ -801,18 +825,27 @@ lr_sweep(Params p) {
       }
       team_sync<TEAM>();
       STAGE(5);
-      // deterministic per-op reduction: warp w handles ops w, w + nwarps, ...
+      // deterministic reduction, four trainable ops per warp pass: strided lane sums then an
+      // xor tree; lane 0 writes the op's partial gradient slot
       {
         const int warp = tid >> 5, lane = tid & 31;
         constexpr int NW = TEAM / 32;
-        for (int oi = warp; oi < nops; oi += NW) {
-          const int tix = oc_tidx(sm.ocode[oi]);
-          if (tix < 0) continue;
-          R s = R(0);
-          for (int k = lane; k < TEAM; k += 32) s += contrib[tix * TEAM + k];
+        for (int t0 = warp * 4; t0 < ntr; t0 += NW * 4) {
+          R sacc[4];
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-          if (lane == 0) gpart[sm.ogidx[oi]] = s;
+          for (int u = 0; u < 4; ++u) {
+            sacc[u] = R(0);
+            if (t0 + u < ntr)
+              for (int k = lane; k < TEAM; k += 32) sacc[u] += contrib[(t0 + u) * TEAM + k];
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], off);
+          if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (t0 + u < ntr) gpart[sm.ogidx[t0 + u]] = sacc[u];
         }
       }
       team_sync<TEAM>();
@@ -919,9 +952,9 @@ inner_sweep(InnerParams p) {
                         reinterpret_cast<int*>(base + p.off_qb), nullptr);
     team_sync<TEAM>();
     fold_site<R, LD, TEAM>(p.ket, sk, tid, reinterpret_cast<C*>(base + p.off_mk), reinterpret_cast<int*>(base + p.off_ok),
-                           Ak, AHk, 31 - __clz(sk.chi_r));
+                           Ak, nullptr, 31 - __clz(sk.chi_r));
     fold_site<R, LD, TEAM>(p.bra, sb, tid, reinterpret_cast<C*>(base + p.off_mb), reinterpret_cast<int*>(base + p.off_ob),
-                           Ab, AHb, 31 - __clz(sb.chi_r));
+                           Ab, nullptr, 31 - __clz(sb.chi_r));
     team_sync<TEAM>();
     // T[s] = L * Ak[s]
     gemm_group<C, LD, TEAM>(tid, 2, sb.chi_l, sk.chi_r, sk.chi_l, 1,
@@ -930,8 +963,8 @@ inner_sweep(InnerParams p) {
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(T + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     team_sync<TEAM>();
     // L' = sum_s AHb[s] T[s]
-    gemm_group<C, LD, TEAM>(tid, 1, sb.chi_r, sk.chi_r, sb.chi_l, 2,
-        [&](int, int qq) { return AHb + qq * MS; },
+    gemm_group<C, LD, TEAM, true, false>(tid, 1, sb.chi_r, sk.chi_r, sb.chi_l, 2,
+        [&](int, int qq) { return Ab + qq * MS; },
         [&](int, int qq) { return T + qq * MS; },
         [&](int, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(L + i0 * LD + j, rt, a0, a1, a2, a3); });
     team_sync<TEAM>();
@@ -1006,10 +1039,11 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   const size_t ms = (size_t)LD * LD * csz;
   const int D = c->d_max < 1 ? 1 : c->d_max;
   size_t off = 0;
+  const bool fused = chi <= 8 && D <= 4 && (!lr || mode == 0);   // kernels: FUSE && D <= FDM
   L.a = (int32_t)off; off += 2 * ms;
-  L.ah = (int32_t)off; off += 2 * ms;
+  L.ah = L.a;                                        // conjugate transposes are read in place
   L.env = (int32_t)off; off += (size_t)D * ms;       // RL: P in/out; LR: Lambda
-  L.m = (int32_t)off; off += (size_t)2 * D * ms;     // RL: N; LR: M (G aliases)
+  L.m = (int32_t)off; off += (size_t)(fused ? (lr ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
   L.pin = (int32_t)off;
   if (lr) off += (size_t)D * ms;
@@ -1040,7 +1074,7 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
     // scratch in the M/BR slots: free during the fold; the gradient sweep rebuilds the levels
     // for its adjoint after G (which occupies the first two M slots)
     const size_t skip = (lr && mode == 0) ? 2 * ms : 0;
-    const size_t avail = (size_t)4 * D * ms - skip;
+    const size_t avail = (size_t)(L.br - L.m) + (size_t)2 * D * ms - skip;
     if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + skip); L.ubuf = (int32_t)(L.lev + lev_bytes); }
     else { L.tree = 0; L.lev = 0; L.ubuf = 0; }
   }
@@ -1180,7 +1214,7 @@ static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
   const size_t csz = 2 * sizeof(R), ms = (size_t)(CHI + 1) * (CHI + 1) * csz;
   size_t off = 0;
   auto take = [&](size_t bytes) { const int32_t o = (int32_t)off; off = align_up(off + bytes, 16); return o; };
-  ip.off_ak = take(2 * ms); ip.off_ahk = take(2 * ms); ip.off_ab = take(2 * ms); ip.off_ahb = take(2 * ms);
+  ip.off_ak = take(2 * ms); ip.off_ab = take(2 * ms); ip.off_ahk = ip.off_ak; ip.off_ahb = ip.off_ab;
   ip.off_t = take(2 * ms); ip.off_l = take(ms);
   ip.off_mk = take((size_t)ip.ket.max_lmat * 4 * csz); ip.off_ik = take((size_t)ip.ket.max_lmat * 4);
   ip.off_pk = take((size_t)ip.ket.max_lmat * sizeof(R)); ip.off_ok = take((size_t)(ip.ket.max_ops + 1) * 4);
