@@ -203,8 +203,9 @@ def run_ours(args, cfg):
     circuit = layered_circuit(n, cfg.layers, cfg.rot, cfg.ent)
     ham_full = tfim(n)
     if sharded and ws > 1:
-        lo, hi = rank * n // ws, (rank + 1) * n // ws
-        ham = PauliHamiltonian(n, tuple(t for t in ham_full.terms if lo <= t.support[0] < hi))
+        from paper_2112_10239_b200.distributed import shard_hamiltonian
+
+        ham = shard_hamiltonian(ham_full, rank, ws)   # terms owned by this rank's chain range
     else:
         ham = ham_full
     seed = 0 if sharded else rank
