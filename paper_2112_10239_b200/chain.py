@@ -146,6 +146,23 @@ def split_two_qubit(matrix: np.ndarray):
     return bits, f0, f1
 
 
+def gate_array(g) -> np.ndarray:
+    """A gate's matrix as ndarray (this package's Gate or tnsim's DenseTensor-backed Gate)."""
+    m = g.matrix
+    return np.asarray(m.array if hasattr(m, "array") else m, dtype=complex)
+
+
+def structure_key(circuit):
+    """Hashable key of everything but trainable angle values (plan cache key); works for
+    this package's Circuit and for reference tnsim.Circuit objects."""
+    if hasattr(circuit, "structure_key"):
+        return circuit.structure_key()
+    tr = set(circuit.trainable)
+    parts = tuple((g.name, tuple(g.wires), "T" if i in tr else gate_array(g).tobytes())
+                  for i, g in enumerate(circuit.gates))
+    return (circuit.n_qubits, parts, tuple(circuit.trainable))
+
+
 def time_gates(circuit) -> list:
     """Circuit (reference-compatible object) -> list[TimeGate] in gate order."""
     slot_of = {gi: s for s, gi in enumerate(circuit.trainable)}
@@ -162,7 +179,7 @@ def time_gates(circuit) -> list:
                     raise InputError(f"trainable gate '{g.name}' is not a rotation")
                 spec = MatSpec(ROT_KIND[g.name], slot_of[gi])
             else:
-                spec = MatSpec.of(np.asarray(g.matrix))
+                spec = MatSpec.of(gate_array(g))
             out.append(TimeGate(wires[0], wires[0], 0, [spec], []))
             continue
         if len(wires) != 2:
@@ -174,7 +191,7 @@ def time_gates(circuit) -> list:
             bits, f0 = 1, [MatSpec.of(_P0), MatSpec.of(_P1)]
             f1 = [MatSpec.of(_I2), MatSpec(KIND_RZ, slot_of[gi])]
         else:
-            bits, m0, m1 = split_two_qubit(np.asarray(g.matrix))
+            bits, m0, m1 = split_two_qubit(gate_array(g))
             f0 = [MatSpec.of(x) for x in m0]
             f1 = [MatSpec.of(x) for x in m1]
         if bits == 0:  # product gate: two single-site factors

@@ -55,7 +55,7 @@ def device_plan(circuit, terms, mode: str, batch: int, device, segments=None, in
         raise InputError("the B200 engine runs on CUDA devices only")
     supports = tuple(ops for _, ops in terms)
     if segments is None:
-        skey = (circuit.structure_key(), supports, int(batch))
+        skey = (C.structure_key(circuit), supports, int(batch))
         seg_key = _SEGS.get(skey)
         if seg_key is None:
             seg_key = C.choose_segments(circuit.n_qubits, terms, C.time_gates(circuit), batch)
@@ -63,7 +63,7 @@ def device_plan(circuit, terms, mode: str, batch: int, device, segments=None, in
     else:
         seg_key = segments
     init_key = None if init is None else np.asarray(init, dtype=complex).tobytes()
-    key = (circuit.structure_key(), supports, mode, seg_key, init_key,
+    key = (C.structure_key(circuit), supports, mode, seg_key, init_key,
            dev.index if dev.index is not None else torch.cuda.current_device(), dtype)
     dp = _PLANS.get(key)
     if dp is None:

@@ -120,3 +120,31 @@ def test_every_module_imports_without_a_gpu():
     for m in ("autodiff", "chain", "circuits", "engine", "errors", "hamiltonians", "maxcut", "program",
               "roofline", "seeding", "tlq", "workloads", "_lib", "build"):
         importlib.import_module(f"paper_2112_10239_b200.{m}")
+
+
+def test_reference_objects_compile_directly():
+    """A tnsim maintainer passes tnsim.Circuit / PauliHamiltonian straight to the engine
+    (INTEGRATION.md); the compiler duck-types them.  Build container only."""
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted")
+    import sys
+
+    sys.path.insert(0, ref)
+    try:
+        import tnsim
+    finally:
+        sys.path.remove(ref)
+    import mirror
+
+    c = tnsim.Circuit(6, tuple(tnsim.standard_gate(*g) for g in (("ry", (0,), 0.3), ("cnot", (0, 1)), ("rx", (2,), 0.1),
+                                                                   ("cz", (1, 2)), ("ry", (5,), 0.7), ("crz", (4, 5), 0.2))),
+                      trainable=(0, 2, 4, 5))
+    h = tnsim.tfim(6)
+    terms = C.normalize_terms(h)
+    plan = C.compile_chain(c, terms, "energy", segments=2)
+    th = np.array([0.3, 0.1, 0.7, 0.2])
+    e, g = mirror.energy_grad(plan, th, np.array([t[0].real for t in terms]))
+    v, gr = tnsim.grad_expval(c, h, th, engine="tt")
+    assert abs(e.real - v) < 1e-12 and np.max(np.abs(g - gr)) < 1e-12
+    assert C.structure_key(c) == C.structure_key(c)
