@@ -109,6 +109,12 @@ typedef struct {
   const int32_t* gred_ptr;
   const int32_t* gred_idx;
   const int32_t* term_active; /* [n_terms] 0 for identity terms (value 1) */
+  /* Per-site descriptor blobs (16-byte units), prefetched with cp.async one site ahead:
+   * [header {len, next_rl, next_lr, 0}] [tq_site] [ops: {opcode, gidx, tbase, 0}]
+   * [factor entries: complex64 3 units / complex128 6 units] [rl edges] [lr edges]. */
+  const void* blob;
+  const int32_t* blob_off;    /* [n_sites] offset of each site's blob (16-byte units) */
+  int32_t blob_max, blob_dtype; /* largest blob (units); dtype the entries were packed for */
 } tq_chain;
 
 /* Bytes of device workspace one call needs. */

@@ -39,6 +39,8 @@ class TqChain(ctypes.Structure):
         ("edges", ctypes.c_void_p), ("fins", ctypes.c_void_p), ("passes", ctypes.c_void_p),
         ("segs", ctypes.c_void_p), ("gred_ptr", ctypes.c_void_p), ("gred_idx", ctypes.c_void_p),
         ("term_active", ctypes.c_void_p),
+        ("blob", ctypes.c_void_p), ("blob_off", ctypes.c_void_p),
+        ("blob_max", ctypes.c_int32), ("blob_dtype", ctypes.c_int32),
     ]
 
 
@@ -115,10 +117,87 @@ NUMPY_SIZES = [C.SITE_DTYPE.itemsize, C.OP_DTYPE.itemsize, C.MAT_DTYPE.itemsize,
                C.PASS_DTYPE.itemsize, C.SEG_DTYPE.itemsize, ctypes.sizeof(TqChain)]
 
 
+def pack_opcode(ops: np.ndarray) -> np.ndarray:
+    """Kernel op code: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24] toff[24:29]."""
+    return (ops["lmat"] | (ops["src"] << 9) | (ops["shift"] << 11) | (ops["bits"] << 16)
+            | ((ops["tidx"] + 1) << 18) | (ops["toff"] << 24)).astype(np.int32)
+
+
+def build_blobs(plan: C.ChainPlan, dtype_code: int):
+    """Per-site descriptor blobs (layout in include/tq_engine.h); returns (bytes, offsets, max)."""
+    eu = 3 if dtype_code == TQ_C64 else 6
+    rdt = np.float32 if dtype_code == TQ_C64 else np.float64
+    sites, ops, mats, edges = plan.sites, plan.ops, plan.mats, plan.edges
+    nsite = len(sites)
+    lens = np.zeros(nsite, dtype=np.int64)
+    for i in range(nsite):
+        st = sites[i]
+        lens[i] = 1 + 8 + int(st["op_count"]) + eu * int(st["lmat_count"]) + int(st["rl_edge_count"]) + int(st["lr_edge_count"])
+    offs = np.zeros(nsite, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)[:-1]
+    total = int(lens.sum()) if nsite else 1
+    bmax = int(lens.max()) if nsite else 1
+    buf = np.zeros((total + bmax) * 16, dtype=np.uint8)   # tail padding: prefetches copy bmax units
+    nxt_rl = np.full(nsite, -1, dtype=np.int64)
+    nxt_lr = np.full(nsite, -1, dtype=np.int64)
+    for sg in plan.segs:
+        b0, cnt = int(sg["site_begin"]), int(sg["site_count"])
+        for k in range(cnt):
+            i = b0 + k
+            if k > 0:
+                nxt_rl[i] = offs[i - 1]
+            if k + 1 < cnt:
+                nxt_lr[i] = offs[i + 1]
+    opc = pack_opcode(ops) if len(ops) else np.zeros(0, np.int32)
+    for i in range(nsite):
+        st = sites[i]
+        base = int(offs[i]) * 16
+        hdr = np.array([lens[i], nxt_rl[i], nxt_lr[i], 0], dtype=np.int32)
+        buf[base:base + 16] = hdr.view(np.uint8)
+        buf[base + 16:base + 144] = np.frombuffer(st.tobytes(), dtype=np.uint8)
+        o = base + 144
+        ob, oc = int(st["op_begin"]), int(st["op_count"])
+        if oc:
+            rec = np.zeros((oc, 4), dtype=np.int32)
+            rec[:, 0] = opc[ob:ob + oc]
+            rec[:, 1] = ops["gidx"][ob:ob + oc]
+            rec[:, 2] = ops["tbase"][ob:ob + oc]
+            rec[:, 3] = ops["tidx"][ob:ob + oc]
+            buf[o:o + 16 * oc] = rec.view(np.uint8).reshape(-1)
+            o += 16 * oc
+        eb, ec = int(st["ent_begin"]), int(st["lmat_count"])
+        if ec:
+            m = mats[eb:eb + ec]
+            if dtype_code == TQ_C64:
+                rec = np.zeros((ec, 12), dtype=np.int32)
+                rec[:, 0] = m["kind"] | (m["cls"] << 8)
+                rec[:, 1] = m["slot"]
+                f = rec.view(np.float32)
+                f[:, 2] = (1.0 / m["pscale"]).astype(np.float32)
+                f[:, 3] = m["angle"].astype(np.float32)
+                f[:, 4:12] = m["m"].astype(np.float32)
+            else:
+                rec = np.zeros((ec, 24), dtype=np.int32)
+                rec[:, 0] = m["kind"] | (m["cls"] << 8)
+                rec[:, 1] = m["slot"]
+                f = rec.view(np.float64)
+                f[:, 1] = 1.0 / m["pscale"]
+                f[:, 2] = m["angle"]
+                f[:, 3:11] = m["m"]
+            buf[o:o + 16 * eu * ec] = rec.view(np.uint8).reshape(-1)
+            o += 16 * eu * ec
+        for key in ("rl", "lr"):
+            b, c = int(st[f"{key}_edge_begin"]), int(st[f"{key}_edge_count"])
+            if c:
+                buf[o:o + 16 * c] = np.frombuffer(edges[b:b + c].tobytes(), dtype=np.uint8)
+                o += 16 * c
+    return buf, offs.astype(np.int32), bmax
+
+
 class DevicePlan:
     """A ChainPlan uploaded to one CUDA device (tables live in torch uint8 tensors)."""
 
-    def __init__(self, plan: C.ChainPlan, device):
+    def __init__(self, plan: C.ChainPlan, device, dtype: str = "complex64"):
         import torch
 
         if not torch.cuda.is_available():
@@ -162,6 +241,12 @@ class DevicePlan:
         ch.gred_ptr = up("gred_ptr", plan.gred_ptr)
         ch.gred_idx = up("gred_idx", plan.gred_idx)
         ch.term_active = up("term_active", plan.term_active)
+        code = TQ_C64 if dtype == "complex64" else TQ_C128
+        blob, boff, bmax = build_blobs(plan, code)
+        ch.blob = up("blob", blob)
+        ch.blob_off = up("blob_off", boff)
+        ch.blob_max = bmax
+        ch.blob_dtype = code
         self.chain = ch
         self._ws = {}
 

@@ -58,6 +58,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, obase, sedge;
   int32_t tree;          // 0: per-pair column walks; 1: digit tree, dedicated levels; 2: digit tree in M/BR scratch
   int32_t lev, ubuf;     // digit-tree level storage and the adjoint's ping-pong buffers
+  int32_t raw0, raw1;    // descriptor-blob double buffer
   int32_t team_bytes;
 };
 
@@ -159,6 +160,66 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
   }
 }
 
+
+// ------------------------------------------------------------------ descriptor blobs
+// One site's descriptors live in a contiguous 16-byte-aligned blob (include/tq_engine.h);
+// the sweeps copy the NEXT site's blob into a shared-memory double buffer with cp.async
+// while the current site computes, so descriptor staging never waits on global memory.
+__device__ __forceinline__ void blob_prefetch(int4* dst, const int4* src, int units, int tid, int team) {
+  for (int c = tid; c < units; c += team) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(saddr), "l"(src + c) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void blob_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename R, int TEAM>
+__device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_row, const R* coef_row, bool rl, int tid,
+                           typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
+                           SEdge<R>* sedge) {
+  using C = typename CT<R>::T;
+  constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
+  constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
+  const int4* ops = raw + 9;
+  const int4* ents = ops + st.op_count;
+  const int4* edg = ents + EU * st.lmat_count + (rl ? 0 : st.rl_edge_count);
+  for (int o = tid; o < st.op_count; o += TEAM) {
+    const int4 r = ops[o];
+    ocode[o] = r.x;
+    obase[o] = r.z;
+    if (r.w >= 0) ogidx[r.w] = r.y;
+  }
+  for (int e = tid; e < st.lmat_count; e += TEAM) {
+    const int* ip = reinterpret_cast<const int*>(ents + EU * e);
+    const R* rp = reinterpret_cast<const R*>(ents + EU * e);
+    const int kind = ip[0] & 0xff, slot = ip[1];
+    C m00, m01, m10, m11;
+    if (kind == 0) {
+      const R* m = rp + FO + 2;
+      m00 = cmk<C>(m[0], m[1]); m01 = cmk<C>(m[2], m[3]); m10 = cmk<C>(m[4], m[5]); m11 = cmk<C>(m[6], m[7]);
+    } else {
+      const R t = slot >= 0 ? theta_row[slot] : rp[FO + 1];
+      R sn, cs;
+      if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); sn = R(sf); cs = R(cf); }
+      else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); sn = R(sd); cs = R(cd); }
+      const R z = R(0);
+      if (kind == 1) { m00 = cmk<C>(cs, z); m01 = cmk<C>(z, -sn); m10 = cmk<C>(z, -sn); m11 = cmk<C>(cs, z); }
+      else if (kind == 2) { m00 = cmk<C>(cs, z); m01 = cmk<C>(-sn, z); m10 = cmk<C>(sn, z); m11 = cmk<C>(cs, z); }
+      else { m00 = cmk<C>(cs, -sn); m01 = cmk<C>(z, z); m10 = cmk<C>(z, z); m11 = cmk<C>(cs, sn); }
+    }
+    mres[4 * e + 0] = m00; mres[4 * e + 1] = m01; mres[4 * e + 2] = m10; mres[4 * e + 3] = m11;
+    minfo[e] = ip[0];
+    mps[e] = rp[FO];
+  }
+  const int ec = rl ? st.rl_edge_count : st.lr_edge_count;
+  for (int ei = tid; ei < ec; ei += TEAM) {
+    const int4 r = edg[ei];
+    SEdge<R> se; se.a = r.x; se.b = r.y; se.op = r.z; se.coef = r.w < 0 ? R(1) : coef_row[r.w];
+    sedge[ei] = se;
+  }
+}
+
 __device__ __forceinline__ bool pass_ok(const tq_chain& ch, const tq_site& st, int al, int be) {
   for (int i = 0; i < st.pass_count; ++i) {
     const tq_pass ps = ch.passes[st.pass_begin + i];
@@ -180,6 +241,7 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
     C v1 = cmk<C>(R(st.init[2]), R(st.init[3]));
     if (st.pass_count && !pass_ok(ch, st, al, be)) { v0 = cmk<C>(R(0), R(0)); v1 = v0; }
     else {
+#pragma unroll 4
       for (int oi = 0; oi < st.op_count; ++oi) {
         const int c = ocode[oi];
         const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al, be));
@@ -336,6 +398,58 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
     }
   }
   team_sync<TEAM>();
+}
+
+
+// Column adjoint for one (alpha, beta) pair with the whole forward walk held in registers
+// (columns of at most NR ops; fully unrolled so every index is static).
+template <typename R, int NR>
+__device__ __forceinline__ void pair_adjoint_reg(int nops, int al, int be, const int* ocode,
+                                                 const typename CT<R>::T* mres, const int* minfo,
+                                                 typename CT<R>::T i0, typename CT<R>::T i1,
+                                                 typename CT<R>::T u0, typename CT<R>::T u1,
+                                                 R* contrib, int tid, int team, bool one_pair) {
+  using C = typename CT<R>::T;
+  C v0[NR + 1], v1[NR + 1];
+  int ent[NR];
+  v0[0] = i0; v1[0] = i1;
+#pragma unroll
+  for (int l = 0; l < NR; ++l) {
+    if (l < nops) {
+      const int c = ocode[l];
+      ent[l] = oc_lmat(c) + oc_digit(c, al, be);
+      const C* M = mres + 4 * ent[l];
+      C n0 = cmul(M[0], v0[l]); cfma(n0, M[1], v1[l]);
+      C n1 = cmul(M[2], v0[l]); cfma(n1, M[3], v1[l]);
+      v0[l + 1] = n0; v1[l + 1] = n1;
+    } else {
+      ent[l] = 0; v0[l + 1] = v0[l]; v1[l + 1] = v1[l];
+    }
+  }
+#pragma unroll
+  for (int l = NR - 1; l >= 0; --l) {
+    if (l < nops) {
+      const int c = ocode[l];
+      const int tix = oc_tidx(c);
+      const int kind = minfo[ent[l]] & 0xff;
+      if (tix >= 0 && kind != 0) {
+        const C a0 = v0[l + 1], a1 = v1[l + 1];
+        C s0, s1;
+        if (kind == 1) { s0 = a1; s1 = a0; }
+        else if (kind == 2) { s0 = cmk<C>(a1.y, -a1.x); s1 = cmk<C>(-a0.y, a0.x); }
+        else { s0 = a0; s1 = cmk<C>(-a1.x, -a1.y); }
+        C d = cmk<C>(R(0), R(0));
+        cfmac(d, u0, s0); cfmac(d, u1, s1);
+        if (one_pair) contrib[tix * team + tid] = d.y;
+        else contrib[tix * team + tid] += d.y;
+      }
+      const C* M = mres + 4 * ent[l];
+      C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+      cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
+      cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
+      u0 = w0; u1 = w1;
+    }
+  }
 }
 
 // Register-tiled complex GEMM over a group of equally shaped tasks:
@@ -614,17 +728,26 @@ rl_sweep(Params p) {
 
   const tq_segment seg = p.c.segs[g];
   C* env_g = reinterpret_cast<C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
+  const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
+  int4* raw[2] = {reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0),
+                  reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1)};
+  blob_prefetch(raw[0], blob + p.c.blob_off[seg.site_begin + seg.site_count - 1], p.c.blob_max, tid, TEAM);
   if (tid == 0) {
     PIN[0] = cmk<C>(R(1), R(0));   // DONE channel = [[1]] at the right end
     const tq_site last = p.c.sites[seg.site_begin + seg.site_count - 1];
     if (p.store_env && last.env_in >= 0) env_g[last.env_in] = PIN[0];
   }
-  for (int q = seg.site_count - 1; q >= 0; --q) {
-    const tq_site st = p.c.sites[seg.site_begin + q];
+  int cur = 0;
+  for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
+    blob_wait();
+    team_sync<TEAM>();
+    const tq_site st = *reinterpret_cast<const tq_site*>(raw[cur] + 1);
+    const int nxt = raw[cur][0].y;
+    if (nxt >= 0) blob_prefetch(raw[cur ^ 1], blob + nxt, p.c.blob_max, tid, TEAM);
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
-    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, true, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
+    stage_blob<R, TEAM>(raw[cur], st, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     team_sync<TEAM>();
     STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
@@ -701,13 +824,22 @@ lr_sweep(Params p) {
   const C* env_g = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
   R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
   if (tid == 0) LAM[0] = cmk<C>(R(1), R(0));
-  for (int q = 0; q < seg.site_count; ++q) {
-    const tq_site st = p.c.sites[seg.site_begin + q];
+  const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
+  int4* raw[2] = {reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0),
+                  reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1)};
+  blob_prefetch(raw[0], blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
+  int cur = 0;
+  for (int q = 0; q < seg.site_count; ++q, cur ^= 1) {
+    blob_wait();
+    team_sync<TEAM>();
+    const tq_site st = *reinterpret_cast<const tq_site*>(raw[cur] + 1);
+    const int nxt = raw[cur][0].z;
+    if (nxt >= 0) blob_prefetch(raw[cur ^ 1], blob + nxt, p.c.blob_max, tid, TEAM);
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = p.mode == 0 ? st.rl_db : 1;
-    stage_site<R, TEAM>(p.c, theta_b, coef_b, st, tid, false, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
+    stage_blob<R, TEAM>(raw[cur], st, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
@@ -765,7 +897,16 @@ lr_sweep(Params p) {
         tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
         tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
       }
-      for (int pi = tid; pi < npair; pi += TEAM) {
+      if (nops <= 16) {
+        for (int pi = tid; pi < npair; pi += TEAM) {
+          const int al = pi >> lcr, be = pi & (cr - 1);
+          if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
+          pair_adjoint_reg<R, 16>(nops, al, be, sm.ocode, sm.mres, sm.minfo,
+                                  cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
+                                  G[al * LD + be], G[MS + al * LD + be], contrib, tid, TEAM, one_pair);
+        }
+      }
+      for (int pi = tid; nops > 16 && pi < npair; pi += TEAM) {
         const int al = pi >> lcr, be = pi & (cr - 1);
         if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
         C sv[MAXSAVE];
@@ -1062,6 +1203,8 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.ogidx = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.obase = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.sedge = (int32_t)off; off += align_up((size_t)(c->max_edges > 0 ? c->max_edges : 1) * (rsz == 8 ? 24 : 16), 16);
+  L.raw0 = (int32_t)off; off += (size_t)c->blob_max * 16;
+  L.raw1 = (int32_t)off; off += (size_t)c->blob_max * 16;
   // digit tree: levels (+ adjoint ping-pong buffers in the gradient sweep)
   const size_t lev_bytes = align_up((size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz, 16);
   const size_t u_bytes = (lr && mode == 0) ? (size_t)2 * chi * chi * 2 * csz : 0;
@@ -1151,6 +1294,7 @@ static tq_status dispatch(Params& prm, bool run_lr, cudaStream_t s) {
 
 static tq_status check_chain(const tq_chain* c, int batch) {
   if (!c) return fail(TQ_ERR_INPUT, "null chain");
+  if (!c->blob || !c->blob_off) return fail(TQ_ERR_INPUT, "chain has no descriptor blobs");
   if (batch < 0) return fail(TQ_ERR_INPUT, "negative batch");
   if (c->chi_max > 32) return fail(TQ_ERR_UNSUPPORTED, "bond dimension exceeds 32");
   return TQ_OK;
@@ -1266,6 +1410,7 @@ tq_status tq_energy_grad(const tq_chain* chain, int32_t dtype, int32_t batch, co
   tq_status st = check_chain(chain, batch);
   if (st != TQ_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (chain->blob_dtype != dtype) return fail(TQ_ERR_INPUT, "chain blobs were packed for a different dtype");
   if (dtype == TQ_C64) return energy_grad_impl<float>(chain, batch, theta, theta_stride, coef, coef_stride, energy, grad, workspace, workspace_bytes, s);
   if (dtype == TQ_C128) return energy_grad_impl<double>(chain, batch, theta, theta_stride, coef, coef_stride, energy, grad, workspace, workspace_bytes, s);
   return fail(TQ_ERR_INPUT, "unknown dtype");
@@ -1276,6 +1421,7 @@ tq_status tq_term_values(const tq_chain* chain, int32_t dtype, int32_t batch, co
   tq_status st = check_chain(chain, batch);
   if (st != TQ_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (chain->blob_dtype != dtype) return fail(TQ_ERR_INPUT, "chain blobs were packed for a different dtype");
   if (dtype == TQ_C64) return values_impl<float>(chain, batch, theta, theta_stride, values, workspace, workspace_bytes, s);
   if (dtype == TQ_C128) return values_impl<double>(chain, batch, theta, theta_stride, values, workspace, workspace_bytes, s);
   return fail(TQ_ERR_INPUT, "unknown dtype");

@@ -70,7 +70,7 @@ def device_plan(circuit, terms, mode: str, batch: int, device, segments=None, in
         limit = C.MAX_CHI if dtype == "complex64" else C.MAX_CHI_F64
         plan = C.compile_chain(circuit, terms, mode=mode, batch=batch, segments=seg_key, init=init,
                                chi_limit=limit)
-        dp = _lib.DevicePlan(plan, dev)
+        dp = _lib.DevicePlan(plan, dev, dtype)
         _PLANS[key] = dp
         while len(_PLANS) > _MAX_PLANS:
             _PLANS.popitem(last=False)
