@@ -703,7 +703,7 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
@@ -729,9 +729,9 @@ rl_sweep(Params p) {
   const tq_segment seg = p.c.segs[g];
   C* env_g = reinterpret_cast<C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
-  int4* raw[2] = {reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0),
-                  reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1)};
-  blob_prefetch(raw[0], blob + p.c.blob_off[seg.site_begin + seg.site_count - 1], p.c.blob_max, tid, TEAM);
+  int4* const raw0 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0);
+  int4* const raw1 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1);
+  blob_prefetch(raw0, blob + p.c.blob_off[seg.site_begin + seg.site_count - 1], p.c.blob_max, tid, TEAM);
   if (tid == 0) {
     PIN[0] = cmk<C>(R(1), R(0));   // DONE channel = [[1]] at the right end
     const tq_site last = p.c.sites[seg.site_begin + seg.site_count - 1];
@@ -741,13 +741,14 @@ rl_sweep(Params p) {
   for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
     blob_wait();
     team_sync<TEAM>();
-    const tq_site st = *reinterpret_cast<const tq_site*>(raw[cur] + 1);
-    const int nxt = raw[cur][0].y;
-    if (nxt >= 0) blob_prefetch(raw[cur ^ 1], blob + nxt, p.c.blob_max, tid, TEAM);
+    const int4* rc = cur ? raw1 : raw0;
+    const tq_site st = *reinterpret_cast<const tq_site*>(rc + 1);
+    const int nxt = rc[0].y;
+    if (nxt >= 0) blob_prefetch(cur ? raw0 : raw1, blob + nxt, p.c.blob_max, tid, TEAM);
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
-    stage_blob<R, TEAM>(raw[cur], st, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
+    stage_blob<R, TEAM>(rc, st, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     team_sync<TEAM>();
     STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
@@ -794,7 +795,7 @@ rl_sweep(Params p) {
 // ------------------------------------------------------------------ left-to-right sweep
 // mode 0: gradient (G + per-pair column adjoint); mode 1: per-term values.
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 lr_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
@@ -825,21 +826,22 @@ lr_sweep(Params p) {
   R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
   if (tid == 0) LAM[0] = cmk<C>(R(1), R(0));
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
-  int4* raw[2] = {reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0),
-                  reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1)};
-  blob_prefetch(raw[0], blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
+  int4* const raw0 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0);
+  int4* const raw1 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1);
+  blob_prefetch(raw0, blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
   int cur = 0;
   for (int q = 0; q < seg.site_count; ++q, cur ^= 1) {
     blob_wait();
     team_sync<TEAM>();
-    const tq_site st = *reinterpret_cast<const tq_site*>(raw[cur] + 1);
-    const int nxt = raw[cur][0].z;
-    if (nxt >= 0) blob_prefetch(raw[cur ^ 1], blob + nxt, p.c.blob_max, tid, TEAM);
+    const int4* rc = cur ? raw1 : raw0;
+    const tq_site st = *reinterpret_cast<const tq_site*>(rc + 1);
+    const int nxt = rc[0].z;
+    if (nxt >= 0) blob_prefetch(cur ? raw0 : raw1, blob + nxt, p.c.blob_max, tid, TEAM);
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = p.mode == 0 ? st.rl_db : 1;
-    stage_blob<R, TEAM>(raw[cur], st, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
+    stage_blob<R, TEAM>(rc, st, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
@@ -1061,7 +1063,7 @@ struct InnerParams {
 };
 
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 inner_sweep(InnerParams p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
