@@ -59,6 +59,8 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t tree;          // 0: per-pair column walks; 1: digit tree, dedicated levels; 2: digit tree in M/BR scratch
   int32_t lev, ubuf;     // digit-tree level storage and the adjoint's ping-pong buffers
   int32_t raw0, raw1;    // descriptor-blob double buffer
+  int32_t dstride;       // bytes between the two resolved-descriptor buffers (mres .. sbuf)
+  int32_t sbuf;          // blob header + tq_site copy inside a resolved-descriptor buffer
   int32_t team_bytes;
 };
 
@@ -177,10 +179,11 @@ __device__ __forceinline__ void blob_wait() { asm volatile("cp.async.wait_group 
 template <typename R, int TEAM>
 __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_row, const R* coef_row, bool rl, int tid,
                            typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
-                           SEdge<R>* sedge) {
+                           SEdge<R>* sedge, int4* sbuf) {
   using C = typename CT<R>::T;
   constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
   constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
+  if (tid < 9) sbuf[tid] = raw[tid];              // header + site struct for the sweep loop
   const int4* ops = raw + 9;
   const int4* ents = ops + st.op_count;
   const int4* edg = ents + EU * st.lmat_count + (rl ? 0 : st.rl_edge_count);
@@ -517,6 +520,7 @@ struct TeamSmem {
   int *minfo, *ocode, *ogidx, *obase;
   C *lev, *ubuf;
   SEdge<R>* sedge;
+  int4* sbuf;
   __device__ TeamSmem(unsigned char* base, const Layout& L) {
     A = reinterpret_cast<C*>(base + L.a); AH = reinterpret_cast<C*>(base + L.ah);
     ENV = reinterpret_cast<C*>(base + L.env); M = reinterpret_cast<C*>(base + L.m);
@@ -527,6 +531,18 @@ struct TeamSmem {
     ogidx = reinterpret_cast<int*>(base + L.ogidx); sedge = reinterpret_cast<SEdge<R>*>(base + L.sedge);
     obase = reinterpret_cast<int*>(base + L.obase);
     lev = reinterpret_cast<C*>(base + L.lev); ubuf = reinterpret_cast<C*>(base + L.ubuf);
+    base_ = base; L_ = &L;
+  }
+  unsigned char* base_;
+  const Layout* L_;
+  // point the descriptor fields at resolved buffer `buf` (0/1)
+  __device__ void sel(int buf) {
+    unsigned char* b = base_ + (size_t)buf * L_->dstride;
+    mres = reinterpret_cast<C*>(b + L_->mres); mps = reinterpret_cast<R*>(b + L_->mps);
+    minfo = reinterpret_cast<int*>(b + L_->minfo); ocode = reinterpret_cast<int*>(b + L_->ocode);
+    ogidx = reinterpret_cast<int*>(b + L_->ogidx); obase = reinterpret_cast<int*>(b + L_->obase);
+    sedge = reinterpret_cast<SEdge<R>*>(b + L_->sedge);
+    sbuf = reinterpret_cast<int4*>(b + L_->sbuf);
   }
 };
 
@@ -737,19 +753,26 @@ rl_sweep(Params p) {
     const tq_site last = p.c.sites[seg.site_begin + seg.site_count - 1];
     if (p.store_env && last.env_in >= 0) env_g[last.env_in] = PIN[0];
   }
+  // prologue: resolve the first site into descriptor buffer 0, then prefetch the second blob
+  blob_wait();
+  team_sync<TEAM>();
+  {
+    const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
+    sm.sel(0);
+    stage_blob<R, TEAM>(raw0, s0, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+    const int nx = raw0[0].y;
+    team_sync<TEAM>();
+    if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
+  }
   int cur = 0;
   for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
-    blob_wait();
     team_sync<TEAM>();
-    const int4* rc = cur ? raw1 : raw0;
-    const tq_site st = *reinterpret_cast<const tq_site*>(rc + 1);
-    const int nxt = rc[0].y;
-    if (nxt >= 0) blob_prefetch(cur ? raw0 : raw1, blob + nxt, p.c.blob_max, tid, TEAM);
+    sm.sel(cur);
+    const tq_site st = *reinterpret_cast<const tq_site*>(sm.sbuf + 1);
+    const bool has_next = sm.sbuf[0].y >= 0;
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
-    stage_blob<R, TEAM>(rc, st, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
-    team_sync<TEAM>();
     STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
@@ -758,6 +781,7 @@ rl_sweep(Params p) {
       // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
       product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, sm.sedge,
                                               st.rl_edge_count, sm.BR);
+      blob_wait();
       team_sync<TEAM>();
       STAGE(2);
     } else {
@@ -769,6 +793,7 @@ rl_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(2);
       bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
+      blob_wait();
       team_sync<TEAM>();
       STAGE(3);
     }
@@ -785,8 +810,17 @@ rl_sweep(Params p) {
             h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
           }
         });
+    // resolve the next site's descriptors while the GEMM above is in flight (independent work)
+    int nx2 = -1;
+    if (has_next) {
+      const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+      nx2 = raw0[0].y;
+      sm.sel(cur ^ 1);
+      stage_blob<R, TEAM>(raw0, sn, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+    }
     team_sync<TEAM>();
     STAGE(4);
+    if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
   }
   if (tid == 0) reinterpret_cast<C*>(p.epart)[(size_t)b * S + g] = PIN[0];
   STAGE_END(0);
@@ -829,19 +863,26 @@ lr_sweep(Params p) {
   int4* const raw0 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0);
   int4* const raw1 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1);
   blob_prefetch(raw0, blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
+  blob_wait();
+  team_sync<TEAM>();
+  {
+    const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
+    sm.sel(0);
+    stage_blob<R, TEAM>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+    const int nx = raw0[0].z;
+    team_sync<TEAM>();
+    if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
+  }
   int cur = 0;
   for (int q = 0; q < seg.site_count; ++q, cur ^= 1) {
-    blob_wait();
     team_sync<TEAM>();
-    const int4* rc = cur ? raw1 : raw0;
-    const tq_site st = *reinterpret_cast<const tq_site*>(rc + 1);
-    const int nxt = rc[0].z;
-    if (nxt >= 0) blob_prefetch(cur ? raw0 : raw1, blob + nxt, p.c.blob_max, tid, TEAM);
+    sm.sel(cur);
+    const tq_site st = *reinterpret_cast<const tq_site*>(sm.sbuf + 1);
+    const bool has_next = sm.sbuf[0].z >= 0;
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = p.mode == 0 ? st.rl_db : 1;
-    stage_blob<R, TEAM>(rc, st, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge);
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
@@ -860,6 +901,7 @@ lr_sweep(Params p) {
       // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
       product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, sm.A, LAM, sm.sedge,
                                               st.lr_edge_count, sm.BR);
+      blob_wait();
       team_sync<TEAM>();
       STAGE(2);
     } else {
@@ -871,6 +913,7 @@ lr_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(2);
       bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
+      blob_wait();
       team_sync<TEAM>();
       STAGE(3);
     }
@@ -879,6 +922,14 @@ lr_sweep(Params p) {
         [&](int, int qq) { return sm.A + qq * MS; },
         [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+    int nx2 = -1;
+    if (has_next) {   // next site's descriptors, overlapped with this site's GEMMs
+      const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+      nx2 = raw0[0].z;
+      sm.sel(cur ^ 1);
+      stage_blob<R, TEAM>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+      sm.sel(cur);
+    }
     if (p.mode == 0) {
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
       gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
@@ -1044,6 +1095,7 @@ lr_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(9);
     }
+    if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
   }
   STAGE_END(1);
 }
@@ -1197,6 +1249,7 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   size_t need = lr ? (size_t)(mode == 0 ? ntr : 8 * D) * team * rsz : 0;
   if (need <= (size_t)2 * D * ms) L.contrib = L.br;
   else { L.contrib = (int32_t)off; off += align_up(need, 16); }
+  off = align_up(off, 16);
   L.mres = (int32_t)off; off += (size_t)c->max_lmat * 4 * csz;
   off = align_up(off, 16);
   L.minfo = (int32_t)off; off += align_up((size_t)c->max_lmat * 4, 16);
@@ -1205,8 +1258,12 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.ogidx = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.obase = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.sedge = (int32_t)off; off += align_up((size_t)(c->max_edges > 0 ? c->max_edges : 1) * (rsz == 8 ? 24 : 16), 16);
-  L.raw0 = (int32_t)off; off += (size_t)c->blob_max * 16;
-  L.raw1 = (int32_t)off; off += (size_t)c->blob_max * 16;
+  off = align_up(off, 16);
+  L.sbuf = (int32_t)off; off += 144;
+  L.dstride = (int32_t)(off - (size_t)L.mres);
+  off += (size_t)L.dstride;                          // second resolved-descriptor buffer
+  L.raw0 = (int32_t)off; off += (size_t)c->blob_max * 16;   // single blob landing buffer
+  L.raw1 = L.raw0;
   // digit tree: levels (+ adjoint ping-pong buffers in the gradient sweep)
   const size_t lev_bytes = align_up((size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz, 16);
   const size_t u_bytes = (lr && mode == 0) ? (size_t)2 * chi * chi * 2 * csz : 0;
