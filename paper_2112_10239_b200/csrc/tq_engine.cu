@@ -383,7 +383,9 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
         cfmac(d, u0, s0); cfmac(d, u1, s1);
         acc += d.y;
       }
-      contrib[tix * TEAM + tid] += acc;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if ((tid & 31) == 0) contrib[tix * (TEAM / 32) + (tid >> 5)] += acc;   // per-warp partials
     }
     if (oi > 0) {
       const int np = 1 << toff;
@@ -403,6 +405,154 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
   team_sync<TEAM>();
 }
 
+
+
+// ------------------------------------------------------------------ grouped digit tree
+// Ops that introduce no new digit act elementwise on the tree index, so a digit op and the
+// non-digit ops after it form one group processed without barriers; each thread carries
+// its (<= EPT) entries in registers through the group.  One team barrier per group.
+constexpr int EPT = 4;
+
+template <typename R, int TEAM>
+__device__ void tree_forward_g(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
+                               const int* obase, typename CT<R>::T* lev) {
+  using C = typename CT<R>::T;
+  const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+  const int nops = st.op_count;
+  int start = 0;
+  while (start < nops) {
+    int end = start + 1;
+    while (end < nops && oc_bits(ocode[end]) == 0) ++end;
+    const int c0 = ocode[start];
+    const int toff = oc_toff(c0), n = 1 << (toff + oc_bits(c0));
+    const int pbase = start ? obase[start - 1] : 0;
+    for (int e = tid; e < n; e += TEAM) {
+      const int idx = e & ((1 << toff) - 1);
+      C v0 = start ? lev[2 * (pbase + idx)] : i0;
+      C v1 = start ? lev[2 * (pbase + idx) + 1] : i1;
+      for (int l = start; l < end; ++l) {
+        const int c = ocode[l];
+        const C* M = mres + 4 * (oc_lmat(c) + (l == start ? (e >> toff) : 0));
+        C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
+        C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
+        v0 = n0; v1 = n1;
+        const int b = obase[l];
+        lev[2 * (b + e)] = v0; lev[2 * (b + e) + 1] = v1;
+      }
+    }
+    team_sync<TEAM>();
+    start = end;
+  }
+}
+
+template <typename R, int LD, int TEAM>
+__device__ void tree_adjoint_g(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                               const int* minfo, const int* ocode, const int* obase, const typename CT<R>::T* lev,
+                               typename CT<R>::T* ubuf, const typename CT<R>::T* G, R* contrib) {
+  using C = typename CT<R>::T;
+  constexpr int MS = LD * LD;
+  constexpr int NW = TEAM / 32;
+  const int nops = st.op_count;
+  if (nops == 0) return;
+  const int clast = ocode[nops - 1];
+  const int nlast = 1 << (oc_toff(clast) + oc_bits(clast));
+  C* cur = ubuf;
+  C* nxt = ubuf + 2 * nlast;
+  int npb = 0;
+  for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
+  for (int e = tid; e < nlast; e += TEAM) {   // U at the last level, gathered from G
+    int al = 0, be = 0;
+    for (int oi = 0; oi < nops; ++oi) {
+      const int c = ocode[oi];
+      const int bits = oc_bits(c);
+      if (!bits) continue;
+      const int d = (e >> oc_toff(c)) & ((1 << bits) - 1);
+      const int src = (c >> 9) & 3, shift = (c >> 11) & 31;
+      if (src == 1) al |= d << shift; else be |= d << shift;
+    }
+    C g0 = cmk<C>(R(0), R(0)), g1 = g0;
+    for (int cmb = 0; cmb < (1 << npb); ++cmb) {
+      int a2 = al, b2 = be, used = 0;
+      for (int i = 0; i < st.pass_count; ++i) {
+        const tq_pass ps = ch.passes[st.pass_begin + i];
+        const int v = (cmb >> used) & ((1 << ps.bits) - 1);
+        a2 |= v << ps.sa; b2 |= v << ps.sb; used += ps.bits;
+      }
+      const C x0 = G[a2 * LD + b2], x1 = G[MS + a2 * LD + b2];
+      g0.x += x0.x; g0.y += x0.y; g1.x += x1.x; g1.y += x1.y;
+    }
+    cur[2 * e] = g0; cur[2 * e + 1] = g1;
+  }
+  bool first = true;
+  int ptoff = 0, pbits = 0;
+  int end = nops;
+  while (end > 0) {
+    int start = end - 1;
+    while (start > 0 && oc_bits(ocode[start]) == 0) --start;
+    team_sync<TEAM>();
+    const int c0 = ocode[start];
+    const int toff = oc_toff(c0), n = 1 << (toff + oc_bits(c0));
+    C u0[EPT], u1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int e = tid + k * TEAM;
+      u0[k] = cmk<C>(R(0), R(0)); u1[k] = u0[k];
+      if (e < n) {
+        if (first) { u0[k] = cur[2 * e]; u1[k] = cur[2 * e + 1]; }
+        else {
+          for (int d = 0; d < (1 << pbits); ++d) {
+            const int ee = e | (d << ptoff);
+            const C a = cur[2 * ee], b2 = cur[2 * ee + 1];
+            u0[k].x += a.x; u0[k].y += a.y; u1[k].x += b2.x; u1[k].y += b2.y;
+          }
+        }
+      }
+    }
+    for (int l = end - 1; l >= start; --l) {
+      const int c = ocode[l];
+      const int tix = oc_tidx(c);
+      const int lm = oc_lmat(c);
+      const C* V = lev + 2 * obase[l];
+      R acc = R(0);
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int e = tid + k * TEAM;
+        if (e >= n) continue;
+        const int ent = lm + (l == start ? (e >> toff) : 0);
+        const int kind = minfo[ent] & 0xff;
+        if (tix >= 0 && kind != 0) {
+          const C v0 = V[2 * e], v1 = V[2 * e + 1];
+          C s0, s1;
+          if (kind == 1) { s0 = v1; s1 = v0; }
+          else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
+          else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
+          C dd = cmk<C>(R(0), R(0));
+          cfmac(dd, u0[k], s0); cfmac(dd, u1[k], s1);
+          acc += dd.y;
+        }
+        const C* M = mres + 4 * ent;
+        C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+        cfmac(w0, M[0], u0[k]); cfmac(w0, M[2], u1[k]);
+        cfmac(w1, M[1], u0[k]); cfmac(w1, M[3], u1[k]);
+        u0[k] = w0; u1[k] = w1;
+      }
+      if (tix >= 0) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if ((tid & 31) == 0) contrib[tix * NW + (tid >> 5)] += acc;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int e = tid + k * TEAM;
+      if (e < n) { nxt[2 * e] = u0[k]; nxt[2 * e + 1] = u1[k]; }
+    }
+    C* t = cur; cur = nxt; nxt = t;
+    first = false; ptoff = toff; pbits = oc_bits(c0);
+    end = start;
+  }
+  team_sync<TEAM>();
+}
 
 // Column adjoint for one (alpha, beta) pair with the whole forward walk held in registers
 // (columns of at most NR ops; fully unrolled so every index is static).
@@ -462,6 +612,44 @@ __device__ __forceinline__ void pair_adjoint_reg(int nops, int al, int be, const
 template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, typename FA, typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
   // CTA: the A operand is stored as X (kk x m) and used as X^H; CTB likewise for B (n x kk).
+  if (LD >= 17 && n >= 16 && m >= 4) {
+    // 4 rows x 2 columns (j, j + n/2) per item: 4 broadcast A loads + 2 B loads per 8 cMAC
+    const int hn = n >> 1;
+    const int lhn = 31 - __clz(hn);
+    const int lmb = (31 - __clz(m)) - 2;
+    const int lper = lmb + lhn;
+    const int total = ntasks << lper;
+    for (int it = tid; it < total; it += TEAM) {
+      const int task = it >> lper;
+      const int r = it & ((1 << lper) - 1);
+      const int j = r & (hn - 1);
+      const int i0 = (r >> lhn) << 2;
+      C c00 = {0, 0}, c10 = {0, 0}, c20 = {0, 0}, c30 = {0, 0};
+      C c01 = {0, 0}, c11 = {0, 0}, c21 = {0, 0}, c31 = {0, 0};
+      for (int q = 0; q < nq; ++q) {
+        const C* Ab = fa(task, q) + (CTA ? i0 : i0 * LD);
+        const C* B0 = fb(task, q) + (CTB ? j * LD : j);
+        const C* B1 = B0 + (CTB ? hn * LD : hn);
+        const int sa = CTA ? LD : 1, ra = CTA ? 1 : LD, sb = CTB ? 1 : LD;
+#pragma unroll 4
+        for (int k = 0; k < kk; ++k) {
+          C b0 = B0[k * sb], b1 = B1[k * sb];
+          if (CTB) { b0 = cconj(b0); b1 = cconj(b1); }
+          const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
+          if (CTA) {
+            cfmac(c00, a0, b0); cfmac(c10, a1, b0); cfmac(c20, a2, b0); cfmac(c30, a3, b0);
+            cfmac(c01, a0, b1); cfmac(c11, a1, b1); cfmac(c21, a2, b1); cfmac(c31, a3, b1);
+          } else {
+            cfma(c00, a0, b0); cfma(c10, a1, b0); cfma(c20, a2, b0); cfma(c30, a3, b0);
+            cfma(c01, a0, b1); cfma(c11, a1, b1); cfma(c21, a2, b1); cfma(c31, a3, b1);
+          }
+        }
+      }
+      store(task, i0, j, 4, c00, c10, c20, c30);
+      store(task, i0, j + hn, 4, c01, c11, c21, c31);
+    }
+    return;
+  }
   const int rt = m >= 4 ? 4 : m;
   const int lrt = rt == 4 ? 2 : (rt == 2 ? 1 : 0);
   const int ln = 31 - __clz(n);
@@ -942,11 +1130,13 @@ lr_sweep(Params p) {
       // projectors discard, then the backward walk accumulating Im<u, sigma v>.
       const int ntr = st.n_train;
       R* contrib = sm.contrib;
-      for (int t = 0; t < ntr; ++t) contrib[t * TEAM + tid] = R(0);
+      const int cw = p.L.tree ? TEAM / 32 : TEAM;      // contribution columns: warps (tree) or threads
+      if (tid < cw) for (int t = 0; t < ntr; ++t) contrib[t * cw + tid] = R(0);
       const int npair = p.L.tree ? 0 : cl * cr;
       const bool one_pair = npair <= TEAM;
       const int nops = st.op_count;
       if (p.L.tree) {
+        team_sync<TEAM>();                            // contrib zeroed before per-warp accumulation
         tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
         tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
       }
@@ -1030,7 +1220,7 @@ lr_sweep(Params p) {
           for (int u = 0; u < 4; ++u) {
             sacc[u] = R(0);
             if (t0 + u < ntr)
-              for (int k = lane; k < TEAM; k += 32) sacc[u] += contrib[(t0 + u) * TEAM + k];
+              for (int k = lane; k < cw; k += 32) sacc[u] += contrib[(t0 + u) * cw + k];
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1)
@@ -1244,10 +1434,13 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   if (lr) off += (size_t)D * ms;
   L.mr = (int32_t)off;
   if (lr && mode == 1) off += (size_t)2 * D * ms;
-  // contrib / value partials: alias the bracket region when it fits
+  // digit tree (gradient sweep, chi >= 16): per-warp contribution partials; adjoint
+  // ping-pong buffers in the M slots after G (free during the adjoint); levels dedicated
+  // when they fit (then the fold builds them and the adjoint reuses them), else in scratch.
   const int ntr = c->max_train > 0 ? c->max_train : 1;
-  size_t need = lr ? (size_t)(mode == 0 ? ntr : 8 * D) * team * rsz : 0;
-  if (need <= (size_t)2 * D * ms) L.contrib = L.br;
+  const bool want_tree = lr && mode == 0 && chi >= 16 && (size_t)chi * chi <= (size_t)4 * team;  // EPT entries/thread
+  size_t need = lr ? (size_t)(mode == 0 ? ntr : 8 * D) * (want_tree ? team / 32 : team) * rsz : 0;
+  if (need <= (size_t)2 * D * ms && !want_tree) L.contrib = L.br;
   else { L.contrib = (int32_t)off; off += align_up(need, 16); }
   off = align_up(off, 16);
   L.mres = (int32_t)off; off += (size_t)c->max_lmat * 4 * csz;
@@ -1264,23 +1457,18 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   off += (size_t)L.dstride;                          // second resolved-descriptor buffer
   L.raw0 = (int32_t)off; off += (size_t)c->blob_max * 16;   // single blob landing buffer
   L.raw1 = L.raw0;
-  // digit tree: levels (+ adjoint ping-pong buffers in the gradient sweep)
   const size_t lev_bytes = align_up((size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz, 16);
-  const size_t u_bytes = (lr && mode == 0) ? (size_t)2 * chi * chi * 2 * csz : 0;
+  const size_t u_bytes = (size_t)2 * chi * chi * 2 * csz;
+  const size_t m_free = (size_t)(L.br - L.m) > 2 * ms ? (size_t)(L.br - L.m) - 2 * ms : 0;  // M slots after G
   const size_t budget = (size_t)227 * 1024 / (team == 32 ? 4 : 1);
-  if (!lr || mode != 0 || chi < 16) {
-    L.tree = 0; L.lev = 0; L.ubuf = 0;   // per-pair walks (the tree's serial levels lose at small chi)
-  } else if (align_up(off + lev_bytes + u_bytes, 128) <= budget) {
-    L.tree = 1; L.lev = (int32_t)off; off += lev_bytes; L.ubuf = (int32_t)off; off += u_bytes;
-  } else {
-    // scratch in the M/BR slots: free during the fold; the gradient sweep rebuilds the levels
-    // for its adjoint after G (which occupies the first two M slots)
-    const size_t skip = (lr && mode == 0) ? 2 * ms : 0;
-    const size_t avail = (size_t)(L.br - L.m) + (size_t)2 * D * ms - skip;
-    if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + skip); L.ubuf = (int32_t)(L.lev + lev_bytes); }
-    else { L.tree = 0; L.lev = 0; L.ubuf = 0; }
+  L.tree = 0; L.lev = 0; L.ubuf = 0;
+  if (want_tree) {
+    (void)m_free; (void)budget;
+    {
+      const size_t avail = (size_t)(L.br - L.m) + (size_t)2 * D * ms - 2 * ms;
+      if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + 2 * ms); L.ubuf = (int32_t)(L.lev + lev_bytes); }
+    }
   }
-  if (L.tree == 2 && L.contrib == L.br) { L.contrib = (int32_t)off; off += align_up(need, 16); }
   L.team_bytes = (int32_t)align_up(off, 128);
   return L;
 }
