@@ -605,6 +605,65 @@ __device__ __forceinline__ void pair_adjoint_reg(int nops, int al, int be, const
   }
 }
 
+
+// Warp-direct variant for one pair per lane (warp teams): every lane walks its pair (zero
+// cotangent when it has none), each trainable op's contributions are summed with an xor tree
+// inside the backward walk and lane 0 writes the partial gradient -- no shared-memory
+// contribution array and no separate reduction stage.
+template <typename R, int NR>
+__device__ __forceinline__ void pair_adjoint_warp(int nops, int al, int be, const int* ocode, const int* ogidx,
+                                                  const typename CT<R>::T* mres, const int* minfo,
+                                                  typename CT<R>::T i0, typename CT<R>::T i1,
+                                                  typename CT<R>::T u0, typename CT<R>::T u1,
+                                                  R* gpart, int lane) {
+  using C = typename CT<R>::T;
+  C v0[NR + 1], v1[NR + 1];
+  int ent[NR], code[NR];
+  v0[0] = i0; v1[0] = i1;
+#pragma unroll
+  for (int l = 0; l < NR; ++l) {
+    if (l < nops) {
+      const int c = ocode[l];
+      code[l] = c;
+      ent[l] = oc_lmat(c) + oc_digit(c, al, be);
+      const C* M = mres + 4 * ent[l];
+      C n0 = cmul(M[0], v0[l]); cfma(n0, M[1], v1[l]);
+      C n1 = cmul(M[2], v0[l]); cfma(n1, M[3], v1[l]);
+      v0[l + 1] = n0; v1[l + 1] = n1;
+    } else {
+      code[l] = 0; ent[l] = 0; v0[l + 1] = v0[l]; v1[l + 1] = v1[l];
+    }
+  }
+#pragma unroll
+  for (int l = NR - 1; l >= 0; --l) {
+    if (l < nops) {
+      const int tix = oc_tidx(code[l]);
+      if (tix >= 0) {   // uniform across the warp
+        const int kind = minfo[ent[l]] & 0xff;
+        R val = R(0);
+        if (kind != 0) {
+          const C a0 = v0[l + 1], a1 = v1[l + 1];
+          C s0, s1;
+          if (kind == 1) { s0 = a1; s1 = a0; }
+          else if (kind == 2) { s0 = cmk<C>(a1.y, -a1.x); s1 = cmk<C>(-a0.y, a0.x); }
+          else { s0 = a0; s1 = cmk<C>(-a1.x, -a1.y); }
+          C d = cmk<C>(R(0), R(0));
+          cfmac(d, u0, s0); cfmac(d, u1, s1);
+          val = d.y;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
+        if (lane == 0) gpart[ogidx[tix]] = val;
+      }
+      const C* M = mres + 4 * ent[l];
+      C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+      cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
+      cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
+      u0 = w0; u1 = w1;
+    }
+  }
+}
+
 // Register-tiled complex GEMM over a group of equally shaped tasks:
 //   C_t[m x n] = sum_{q < nq} A_{t,q}[m x kk] * B_{t,q}[kk x n]   (all row stride LD)
 // Each item computes rt consecutive rows of one column; a warp's lanes walk columns so the
@@ -1130,6 +1189,17 @@ lr_sweep(Params p) {
       // projectors discard, then the backward walk accumulating Im<u, sigma v>.
       const int ntr = st.n_train;
       R* contrib = sm.contrib;
+      if (TEAM == 32 && !p.L.tree && cl * cr <= 32 && st.op_count <= 16) {
+        // one (alpha, beta) pair per lane: warp-direct adjoint + reduction
+        const int al = tid >> lcr, be = tid & (cr - 1);
+        const bool have = tid < cl * cr && !(st.pass_count && !pass_ok(p.c, st, al, be));
+        const C z = cmk<C>(R(0), R(0));
+        pair_adjoint_warp<R, 16>(st.op_count, have ? al : 0, have ? be : 0, sm.ocode, sm.ogidx, sm.mres, sm.minfo,
+                                 cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
+                                 have ? G[al * LD + be] : z, have ? G[MS + al * LD + be] : z, gpart, tid);
+        team_sync<TEAM>();
+        STAGE(5);
+      } else {
       const int cw = p.L.tree ? TEAM / 32 : TEAM;      // contribution columns: warps (tree) or threads
       if (tid < cw) for (int t = 0; t < ntr; ++t) contrib[t * cw + tid] = R(0);
       const int npair = p.L.tree ? 0 : cl * cr;
@@ -1234,6 +1304,7 @@ lr_sweep(Params p) {
       }
       team_sync<TEAM>();
       STAGE(6);
+      }   // per-pair / tree adjoint
     } else {
       // ---- values: rho_a[s'][s] = <A[s'], M[a][s] R> for every source channel a
       gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cr, 1,
