@@ -108,6 +108,54 @@ def _oracle_eval(args):
     return time.perf_counter() - t0
 
 
+def _oracle_forward(args):
+    n, layers, rot, ent, theta = args
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    import oracle as O
+
+    c = O.ry_cz_layers(n, layers, rot, ent)
+    t0 = time.perf_counter()
+    O.evaluate_expval(c, O.tfim_terms(n), theta, eps=1e-12)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_block(cfg, circuit, n, workers):
+    """CPU oracle port on this host, sized to ~10-30 s of CPU work, in the metric's unit.
+
+    cfg1/cfg2: exact taped E+grad (reference grad_expval engine='tt' eps=0).
+    cfg4: the exact taped gradient is infeasible (eps=0 bond 2^lines = 1024); the reference's
+          exact alternative is the shift rule, 2P+1 forward evaluations, so E+grad/s =
+          forwards/s / (2P + 1) from timed forward evaluate_expval(eps=1e-12) runs.
+    cfg5: forward only -> forwards/s."""
+    from paper_2112_10239_b200.workloads import theta_sets
+
+    if cfg.name in ("cfg4", "cfg5"):
+        k = max(1, min(workers, 4))
+        jobs = [(n, cfg.layers, cfg.rot, cfg.ent, th) for th in theta_sets(circuit.n_params, k, seed=99)]
+        import multiprocessing as mp
+
+        with mp.get_context("fork").Pool(k) as pool:
+            t0 = time.perf_counter()
+            per = pool.map(_oracle_forward, jobs)
+            wall = time.perf_counter() - t0
+        fwd_rate = k / wall
+        if cfg.name == "cfg5":
+            return {"value": fwd_rate, "unit": "evals/s", "cores": k, "kind": "port",
+                    "sample": f"{k} forward evaluations n={n} (oracle port of tnsim evaluate_expval eps=1e-12), "
+                              f"{sum(per):.1f} CPU-s"}
+        P = circuit.n_params
+        return {"value": fwd_rate / (2 * P + 1), "unit": "evals/s", "cores": k, "kind": "port",
+                "sample": f"{k} forward evaluations n={n} (evaluate_expval eps=1e-12, {sum(per):.1f} CPU-s); "
+                          f"E+grad via the exact shift rule = {2 * P + 1} forwards per evaluation"}
+    sample_n = min(256, max(2 * workers, 16))
+    rate, wall, cpu_s = cpu_oracle_rate(cfg, theta_sets(circuit.n_params, sample_n, seed=99), workers)
+    return {"value": rate, "unit": "evals/s", "cores": workers, "kind": "port",
+            "sample": f"{sample_n} theta-sets of {cfg.name} (oracle port of tnsim grad_expval engine='tt' eps=0), "
+                      f"{cpu_s:.1f} CPU-s over {wall:.1f} s wall"}
+
+
 def cpu_oracle_rate(cfg, thetas, workers):
     """Evaluate theta-sets with the CPU oracle port on `workers` processes; returns evals/s."""
     import multiprocessing as mp
@@ -343,12 +391,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        cores = host_cores()
-        sample_n = min(256, max(2 * cores, 16))
-        rate, wall, cpu_s = cpu_oracle_rate(cfg, theta_sets(circuit.n_params, sample_n, seed=99), cores)
-        cpu = {"value": rate, "unit": "evals/s", "cores": cores, "kind": "port",
-               "sample": f"{sample_n} theta-sets of {cfg.name} (oracle port of tnsim grad_expval engine='tt' eps=0), "
-                         f"{cpu_s:.1f} CPU-s over {wall:.1f} s wall"}
+        cpu = cpu_baseline_block(cfg, circuit, n, host_cores())
 
     launches_per_step = 2 + (2 if cfg.grad else 0)  # rl_sweep+reduce_energy (+ lr_sweep+reduce_grad)
     line = {

@@ -407,205 +407,6 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
 
 
 
-// ------------------------------------------------------------------ grouped digit tree
-// Ops that introduce no new digit act elementwise on the tree index, so a digit op and the
-// non-digit ops after it form one group processed without barriers; each thread carries
-// its (<= EPT) entries in registers through the group.  One team barrier per group.
-constexpr int EPT = 4;
-
-template <typename R, int TEAM>
-__device__ void tree_forward_g(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
-                               const int* obase, typename CT<R>::T* lev) {
-  using C = typename CT<R>::T;
-  const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
-  const int nops = st.op_count;
-  int start = 0;
-  while (start < nops) {
-    int end = start + 1;
-    while (end < nops && oc_bits(ocode[end]) == 0) ++end;
-    const int c0 = ocode[start];
-    const int toff = oc_toff(c0), n = 1 << (toff + oc_bits(c0));
-    const int pbase = start ? obase[start - 1] : 0;
-    for (int e = tid; e < n; e += TEAM) {
-      const int idx = e & ((1 << toff) - 1);
-      C v0 = start ? lev[2 * (pbase + idx)] : i0;
-      C v1 = start ? lev[2 * (pbase + idx) + 1] : i1;
-      for (int l = start; l < end; ++l) {
-        const int c = ocode[l];
-        const C* M = mres + 4 * (oc_lmat(c) + (l == start ? (e >> toff) : 0));
-        C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
-        C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
-        v0 = n0; v1 = n1;
-        const int b = obase[l];
-        lev[2 * (b + e)] = v0; lev[2 * (b + e) + 1] = v1;
-      }
-    }
-    team_sync<TEAM>();
-    start = end;
-  }
-}
-
-template <typename R, int LD, int TEAM>
-__device__ void tree_adjoint_g(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
-                               const int* minfo, const int* ocode, const int* obase, const typename CT<R>::T* lev,
-                               typename CT<R>::T* ubuf, const typename CT<R>::T* G, R* contrib) {
-  using C = typename CT<R>::T;
-  constexpr int MS = LD * LD;
-  constexpr int NW = TEAM / 32;
-  const int nops = st.op_count;
-  if (nops == 0) return;
-  const int clast = ocode[nops - 1];
-  const int nlast = 1 << (oc_toff(clast) + oc_bits(clast));
-  C* cur = ubuf;
-  C* nxt = ubuf + 2 * nlast;
-  int npb = 0;
-  for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
-  for (int e = tid; e < nlast; e += TEAM) {   // U at the last level, gathered from G
-    int al = 0, be = 0;
-    for (int oi = 0; oi < nops; ++oi) {
-      const int c = ocode[oi];
-      const int bits = oc_bits(c);
-      if (!bits) continue;
-      const int d = (e >> oc_toff(c)) & ((1 << bits) - 1);
-      const int src = (c >> 9) & 3, shift = (c >> 11) & 31;
-      if (src == 1) al |= d << shift; else be |= d << shift;
-    }
-    C g0 = cmk<C>(R(0), R(0)), g1 = g0;
-    for (int cmb = 0; cmb < (1 << npb); ++cmb) {
-      int a2 = al, b2 = be, used = 0;
-      for (int i = 0; i < st.pass_count; ++i) {
-        const tq_pass ps = ch.passes[st.pass_begin + i];
-        const int v = (cmb >> used) & ((1 << ps.bits) - 1);
-        a2 |= v << ps.sa; b2 |= v << ps.sb; used += ps.bits;
-      }
-      const C x0 = G[a2 * LD + b2], x1 = G[MS + a2 * LD + b2];
-      g0.x += x0.x; g0.y += x0.y; g1.x += x1.x; g1.y += x1.y;
-    }
-    cur[2 * e] = g0; cur[2 * e + 1] = g1;
-  }
-  bool first = true;
-  int ptoff = 0, pbits = 0;
-  int end = nops;
-  while (end > 0) {
-    int start = end - 1;
-    while (start > 0 && oc_bits(ocode[start]) == 0) --start;
-    team_sync<TEAM>();
-    const int c0 = ocode[start];
-    const int toff = oc_toff(c0), n = 1 << (toff + oc_bits(c0));
-    C u0[EPT], u1[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int e = tid + k * TEAM;
-      u0[k] = cmk<C>(R(0), R(0)); u1[k] = u0[k];
-      if (e < n) {
-        if (first) { u0[k] = cur[2 * e]; u1[k] = cur[2 * e + 1]; }
-        else {
-          for (int d = 0; d < (1 << pbits); ++d) {
-            const int ee = e | (d << ptoff);
-            const C a = cur[2 * ee], b2 = cur[2 * ee + 1];
-            u0[k].x += a.x; u0[k].y += a.y; u1[k].x += b2.x; u1[k].y += b2.y;
-          }
-        }
-      }
-    }
-    for (int l = end - 1; l >= start; --l) {
-      const int c = ocode[l];
-      const int tix = oc_tidx(c);
-      const int lm = oc_lmat(c);
-      const C* V = lev + 2 * obase[l];
-      R acc = R(0);
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const int e = tid + k * TEAM;
-        if (e >= n) continue;
-        const int ent = lm + (l == start ? (e >> toff) : 0);
-        const int kind = minfo[ent] & 0xff;
-        if (tix >= 0 && kind != 0) {
-          const C v0 = V[2 * e], v1 = V[2 * e + 1];
-          C s0, s1;
-          if (kind == 1) { s0 = v1; s1 = v0; }
-          else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
-          else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
-          C dd = cmk<C>(R(0), R(0));
-          cfmac(dd, u0[k], s0); cfmac(dd, u1[k], s1);
-          acc += dd.y;
-        }
-        const C* M = mres + 4 * ent;
-        C w0 = cmk<C>(R(0), R(0)), w1 = w0;
-        cfmac(w0, M[0], u0[k]); cfmac(w0, M[2], u1[k]);
-        cfmac(w1, M[1], u0[k]); cfmac(w1, M[3], u1[k]);
-        u0[k] = w0; u1[k] = w1;
-      }
-      if (tix >= 0) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if ((tid & 31) == 0) contrib[tix * NW + (tid >> 5)] += acc;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int e = tid + k * TEAM;
-      if (e < n) { nxt[2 * e] = u0[k]; nxt[2 * e + 1] = u1[k]; }
-    }
-    C* t = cur; cur = nxt; nxt = t;
-    first = false; ptoff = toff; pbits = oc_bits(c0);
-    end = start;
-  }
-  team_sync<TEAM>();
-}
-
-// Column adjoint for one (alpha, beta) pair with the whole forward walk held in registers
-// (columns of at most NR ops; fully unrolled so every index is static).
-template <typename R, int NR>
-__device__ __forceinline__ void pair_adjoint_reg(int nops, int al, int be, const int* ocode,
-                                                 const typename CT<R>::T* mres, const int* minfo,
-                                                 typename CT<R>::T i0, typename CT<R>::T i1,
-                                                 typename CT<R>::T u0, typename CT<R>::T u1,
-                                                 R* contrib, int tid, int team, bool one_pair) {
-  using C = typename CT<R>::T;
-  C v0[NR + 1], v1[NR + 1];
-  int ent[NR];
-  v0[0] = i0; v1[0] = i1;
-#pragma unroll
-  for (int l = 0; l < NR; ++l) {
-    if (l < nops) {
-      const int c = ocode[l];
-      ent[l] = oc_lmat(c) + oc_digit(c, al, be);
-      const C* M = mres + 4 * ent[l];
-      C n0 = cmul(M[0], v0[l]); cfma(n0, M[1], v1[l]);
-      C n1 = cmul(M[2], v0[l]); cfma(n1, M[3], v1[l]);
-      v0[l + 1] = n0; v1[l + 1] = n1;
-    } else {
-      ent[l] = 0; v0[l + 1] = v0[l]; v1[l + 1] = v1[l];
-    }
-  }
-#pragma unroll
-  for (int l = NR - 1; l >= 0; --l) {
-    if (l < nops) {
-      const int c = ocode[l];
-      const int tix = oc_tidx(c);
-      const int kind = minfo[ent[l]] & 0xff;
-      if (tix >= 0 && kind != 0) {
-        const C a0 = v0[l + 1], a1 = v1[l + 1];
-        C s0, s1;
-        if (kind == 1) { s0 = a1; s1 = a0; }
-        else if (kind == 2) { s0 = cmk<C>(a1.y, -a1.x); s1 = cmk<C>(-a0.y, a0.x); }
-        else { s0 = a0; s1 = cmk<C>(-a1.x, -a1.y); }
-        C d = cmk<C>(R(0), R(0));
-        cfmac(d, u0, s0); cfmac(d, u1, s1);
-        if (one_pair) contrib[tix * team + tid] = d.y;
-        else contrib[tix * team + tid] += d.y;
-      }
-      const C* M = mres + 4 * ent[l];
-      C w0 = cmk<C>(R(0), R(0)), w1 = w0;
-      cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
-      cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
-      u0 = w0; u1 = w1;
-    }
-  }
-}
-
-
 // Warp-direct variant for one pair per lane (warp teams): every lane walks its pair (zero
 // cotangent when it has none), each trainable op's contributions are summed with an xor tree
 // inside the backward walk and lane 0 writes the partial gradient -- no shared-memory
@@ -965,14 +766,14 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
 // ------------------------------------------------------------------ right-to-left sweep
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
-template <typename R, int CHI, int TEAM>
+template <typename R, int CHI, int TEAM, bool FUSED>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
-  constexpr bool FUSE = CHI <= 8;                 // register-fused product+bracket, one element per thread
+  constexpr bool FUSE = FUSED;                    // register-fused product+bracket (host: chi <= 8 && D <= 4)
   constexpr int FDM = 4;                          // channels handled by the fused stages
   constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1024,7 +825,7 @@ rl_sweep(Params p) {
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     STAGE(1);
-    if (FUSE && db <= FDM && da <= FDM) {
+    if constexpr (FUSE) {
       // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
       product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, sm.sedge,
                                               st.rl_edge_count, sm.BR);
@@ -1074,8 +875,9 @@ rl_sweep(Params p) {
 }
 
 // ------------------------------------------------------------------ left-to-right sweep
-// mode 0: gradient (G + per-pair column adjoint); mode 1: per-term values.
-template <typename R, int CHI, int TEAM>
+// MODE 0: gradient (G + column adjoint); MODE 1: per-term values.  Separate instantiations
+// keep each kernel's code small enough for the instruction cache.
+template <typename R, int CHI, int TEAM, int MODE, bool FUSED>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 lr_sweep(Params p) {
   using C = typename CT<R>::T;
@@ -1083,7 +885,7 @@ lr_sweep(Params p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
-  constexpr bool FUSE = CHI <= 8;                 // register-fused product+bracket, one element per thread
+  constexpr bool FUSE = FUSED;                    // register-fused product+bracket (host: chi <= 8 && D <= 4)
   constexpr int FDM = 4;                          // channels handled by the fused stages
   constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1129,7 +931,7 @@ lr_sweep(Params p) {
     const int cl = st.chi_l, cr = st.chi_r;
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
-    const int npin = p.mode == 0 ? st.rl_db : 1;
+    const int npin = MODE == 0 ? st.rl_db : 1;
     // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
     {
       const C* src = env_g + st.env_in;
@@ -1144,7 +946,7 @@ lr_sweep(Params p) {
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     STAGE(1);
-    if (FUSE && p.mode == 0 && da <= FDM && db <= FDM) {
+    if constexpr (FUSE && MODE == 0) {
       // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
       product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, sm.A, LAM, sm.sedge,
                                               st.lr_edge_count, sm.BR);
@@ -1177,7 +979,7 @@ lr_sweep(Params p) {
       stage_blob<R, TEAM>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
       sm.sel(cur);
     }
-    if (p.mode == 0) {
+    if constexpr (MODE == 0) {
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
       gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
           [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
@@ -1189,12 +991,12 @@ lr_sweep(Params p) {
       // projectors discard, then the backward walk accumulating Im<u, sigma v>.
       const int ntr = st.n_train;
       R* contrib = sm.contrib;
-      if (TEAM == 32 && !p.L.tree && cl * cr <= 32 && st.op_count <= 16) {
+      if (TEAM == 32 && CHI <= 8 && cl * cr <= 32 && st.op_count <= 12) {
         // one (alpha, beta) pair per lane: warp-direct adjoint + reduction
         const int al = tid >> lcr, be = tid & (cr - 1);
         const bool have = tid < cl * cr && !(st.pass_count && !pass_ok(p.c, st, al, be));
         const C z = cmk<C>(R(0), R(0));
-        pair_adjoint_warp<R, 16>(st.op_count, have ? al : 0, have ? be : 0, sm.ocode, sm.ogidx, sm.mres, sm.minfo,
+        pair_adjoint_warp<R, 12>(st.op_count, have ? al : 0, have ? be : 0, sm.ocode, sm.ogidx, sm.mres, sm.minfo,
                                  cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
                                  have ? G[al * LD + be] : z, have ? G[MS + al * LD + be] : z, gpart, tid);
         team_sync<TEAM>();
@@ -1205,21 +1007,14 @@ lr_sweep(Params p) {
       const int npair = p.L.tree ? 0 : cl * cr;
       const bool one_pair = npair <= TEAM;
       const int nops = st.op_count;
-      if (p.L.tree) {
-        team_sync<TEAM>();                            // contrib zeroed before per-warp accumulation
-        tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
-        tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
-      }
-      if (nops <= 16) {
-        for (int pi = tid; pi < npair; pi += TEAM) {
-          const int al = pi >> lcr, be = pi & (cr - 1);
-          if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
-          pair_adjoint_reg<R, 16>(nops, al, be, sm.ocode, sm.mres, sm.minfo,
-                                  cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
-                                  G[al * LD + be], G[MS + al * LD + be], contrib, tid, TEAM, one_pair);
+      if constexpr (CHI >= 16) {
+        if (p.L.tree) {
+          team_sync<TEAM>();                          // contrib zeroed before per-warp accumulation
+          tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
+          tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
         }
       }
-      for (int pi = tid; nops > 16 && pi < npair; pi += TEAM) {
+      for (int pi = tid; pi < npair; pi += TEAM) {
         const int al = pi >> lcr, be = pi & (cr - 1);
         if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
         C sv[MAXSAVE];
@@ -1562,8 +1357,8 @@ static WsLayout ws_layout(const tq_chain* c, int batch, int flags, int dtype) {
 struct Timing { cudaEvent_t ev[4]; bool on; };
 static thread_local Timing g_timing = {{nullptr, nullptr, nullptr, nullptr}, false};
 
-template <typename R, int CHI>
-static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
+template <typename R, int CHI, bool FUSED>
+static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
   constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   const int items = prm.batch * prm.c.n_segments;
@@ -1573,9 +1368,9 @@ static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
     q.L = make_layout(&prm.c, CHI, TEAM, sizeof(R), false, prm.mode);
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
-    cudaFuncSetAttribute(rl_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rl_sweep<R, CHI, TEAM, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (g_timing.on) cudaEventRecord(g_timing.ev[0], s);
-    rl_sweep<R, CHI, TEAM><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    rl_sweep<R, CHI, TEAM, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
     if (g_timing.on) cudaEventRecord(g_timing.ev[1], s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
@@ -1585,14 +1380,27 @@ static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
     q.L = make_layout(&prm.c, CHI, TEAM, sizeof(R), true, prm.mode);
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
-    cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (g_timing.on) cudaEventRecord(g_timing.ev[2], s);
-    lr_sweep<R, CHI, TEAM><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    if (prm.mode == 0) {
+      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 0, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      lr_sweep<R, CHI, TEAM, 0, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    } else {
+      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      lr_sweep<R, CHI, TEAM, 1, false><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    }
     if (g_timing.on) cudaEventRecord(g_timing.ev[3], s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
   }
   return TQ_OK;
+}
+
+// The register-fused product+bracket path needs chi <= 8 and at most 4 MPO channels (the
+// shared-memory layout in make_layout makes the same decision).
+template <typename R, int CHI>
+static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
+  if (CHI <= 8 && prm.c.d_max <= 4) return launch_pair_f<R, CHI, CHI <= 8>(prm, run_lr, s);
+  return launch_pair_f<R, CHI, false>(prm, run_lr, s);
 }
 
 template <typename R>
