@@ -157,3 +157,21 @@ def test_error_taxonomy():
     wide = Circuit(8, tuple(standard_gate("cnot", (0, 7)) for _ in range(6)), ())
     with pytest.raises(BondTooLarge):
         AD.evaluate_expval(wide, tfim(8), [])
+
+
+def test_bitwise_determinism_stress():
+    """Races in the pipelined shared-memory stages would show up as run-to-run differences
+    (compute-sanitizer is unavailable on this pool): repeat varied configurations."""
+    cases = [(10, 4, "cnot", 64, None), (24, 10, "cz", 16, 3), (40, 12, "cz", 8, 5), (12, 20, "cz", 4, 2),
+             (30, 7, "cnot", 8, 4)]
+    for n, layers, ent, B, segs in cases:
+        c = layered_circuit(n, layers, "ry", ent)
+        th = theta_sets(c.n_params, B, seed=n)
+        ref = AD.grad_expval(c, tfim(n), th, segments=segs)
+        vref = AD.expectation_values(c, th, [{0: "Z"}, {1: "X", 2: "Y"}, {n - 1: "Z"}], segments=segs)
+        for _ in range(3):
+            again = AD.grad_expval(c, tfim(n), th, segments=segs)
+            np.testing.assert_array_equal(again[0], ref[0])
+            np.testing.assert_array_equal(again[1], ref[1])
+            np.testing.assert_array_equal(
+                AD.expectation_values(c, th, [{0: "Z"}, {1: "X", 2: "Y"}, {n - 1: "Z"}], segments=segs), vref)
