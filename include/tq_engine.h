@@ -61,6 +61,7 @@ typedef struct {
   int32_t n_train, ent_begin; /* ent_begin: first of this site's contiguous tq_mat entries */
   int64_t env_in, env_out;  /* complex offsets of the stored right envs at cut k+1 / cut k (-1: none) */
   double init[4];           /* input product-state vector of this qubit (re,im,re,im) */
+  int64_t a_off, pad1;      /* complex offset of the folded core A[2][chi_l][chi_r] (RL stores, LR reloads) */
 } tq_site;
 
 /* One operator of a column: selects table entry mat + digit (chain.py OP_DTYPE).
@@ -110,7 +111,7 @@ typedef struct {
   const int32_t* gred_idx;
   const int32_t* term_active; /* [n_terms] 0 for identity terms (value 1) */
   /* Per-site descriptor blobs (16-byte units), prefetched with cp.async one site ahead:
-   * [header {len, next_rl, next_lr, 0}] [tq_site] [ops: {opcode, gidx, tbase, 0}]
+   * [header {len, next_rl, next_lr, 0}] [tq_site: 9 units] [ops: {opcode, gidx, tbase, tidx}]
    * [factor entries: complex64 3 units / complex128 6 units] [rl edges] [lr edges]. */
   const void* blob;
   const int32_t* blob_off;    /* [n_sites] offset of each site's blob (16-byte units) */

@@ -123,6 +123,9 @@ def pack_opcode(ops: np.ndarray) -> np.ndarray:
             | ((ops["tidx"] + 1) << 18) | (ops["toff"] << 24)).astype(np.int32)
 
 
+SITE_UNITS = C.SITE_DTYPE.itemsize // 16
+
+
 def build_blobs(plan: C.ChainPlan, dtype_code: int):
     """Per-site descriptor blobs (layout in include/tq_engine.h); returns (bytes, offsets, max)."""
     eu = 3 if dtype_code == TQ_C64 else 6
@@ -132,7 +135,7 @@ def build_blobs(plan: C.ChainPlan, dtype_code: int):
     lens = np.zeros(nsite, dtype=np.int64)
     for i in range(nsite):
         st = sites[i]
-        lens[i] = 1 + 8 + int(st["op_count"]) + eu * int(st["lmat_count"]) + int(st["rl_edge_count"]) + int(st["lr_edge_count"])
+        lens[i] = 1 + SITE_UNITS + int(st["op_count"]) + eu * int(st["lmat_count"]) + int(st["rl_edge_count"]) + int(st["lr_edge_count"])
     offs = np.zeros(nsite, dtype=np.int64)
     offs[1:] = np.cumsum(lens)[:-1]
     total = int(lens.sum()) if nsite else 1
@@ -154,8 +157,8 @@ def build_blobs(plan: C.ChainPlan, dtype_code: int):
         base = int(offs[i]) * 16
         hdr = np.array([lens[i], nxt_rl[i], nxt_lr[i], 0], dtype=np.int32)
         buf[base:base + 16] = hdr.view(np.uint8)
-        buf[base + 16:base + 144] = np.frombuffer(st.tobytes(), dtype=np.uint8)
-        o = base + 144
+        buf[base + 16:base + 16 + 16 * SITE_UNITS] = np.frombuffer(st.tobytes(), dtype=np.uint8)
+        o = base + 16 + 16 * SITE_UNITS
         ob, oc = int(st["op_begin"]), int(st["op_count"])
         if oc:
             rec = np.zeros((oc, 4), dtype=np.int32)

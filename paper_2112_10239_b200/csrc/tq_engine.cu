@@ -164,6 +164,8 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
 
 
 // ------------------------------------------------------------------ descriptor blobs
+constexpr int SITE_UNITS = sizeof(tq_site) / 16;
+static_assert(sizeof(tq_site) % 16 == 0, "tq_site must be a multiple of 16 bytes");
 // One site's descriptors live in a contiguous 16-byte-aligned blob (include/tq_engine.h);
 // the sweeps copy the NEXT site's blob into a shared-memory double buffer with cp.async
 // while the current site computes, so descriptor staging never waits on global memory.
@@ -183,8 +185,8 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
   using C = typename CT<R>::T;
   constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
   constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
-  if (tid < 9) sbuf[tid] = raw[tid];              // header + site struct for the sweep loop
-  const int4* ops = raw + 9;
+  if (tid < 1 + SITE_UNITS) sbuf[tid] = raw[tid];   // header + site struct for the sweep loop
+  const int4* ops = raw + 1 + SITE_UNITS;
   const int4* ents = ops + st.op_count;
   const int4* edg = ents + EU * st.lmat_count + (rl ? 0 : st.rl_edge_count);
   for (int o = tid; o < st.op_count; o += TEAM) {
@@ -824,6 +826,14 @@ rl_sweep(Params p) {
     STAGE(0);
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
+    if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
+      C* ag = env_g + st.a_off;
+      const int np = cl * cr;
+      for (int e = tid; e < 2 * np; e += TEAM) {
+        const int sidx = e >= np, r = e - sidx * np;
+        ag[e] = sm.A[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))];
+      }
+    }
     STAGE(1);
     if constexpr (FUSE) {
       // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
@@ -932,7 +942,7 @@ lr_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = MODE == 0 ? st.rl_db : 1;
-    // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM)
+    // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM), folded core -> A
     {
       const C* src = env_g + st.env_in;
       const int lper = 2 * lcr;
@@ -940,11 +950,15 @@ lr_sweep(Params p) {
         const int ch = e >> lper, r = e & ((1 << lper) - 1);
         PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
       }
+      const C* ag = env_g + st.a_off;
+      const int np = cl * cr;
+      for (int e = tid; e < 2 * np; e += TEAM) {
+        const int sidx = e >= np, r = e - sidx * np;
+        sm.A[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))] = ag[e];
+      }
     }
     team_sync<TEAM>();
     STAGE(0);
-    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
-    team_sync<TEAM>();
     STAGE(1);
     if constexpr (FUSE && MODE == 0) {
       // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
@@ -1318,7 +1332,7 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.obase = (int32_t)off; off += align_up((size_t)(c->max_ops > 0 ? c->max_ops : 1) * 4, 16);
   L.sedge = (int32_t)off; off += align_up((size_t)(c->max_edges > 0 ? c->max_edges : 1) * (rsz == 8 ? 24 : 16), 16);
   off = align_up(off, 16);
-  L.sbuf = (int32_t)off; off += 144;
+  L.sbuf = (int32_t)off; off += 16 + sizeof(tq_site);
   L.dstride = (int32_t)(off - (size_t)L.mres);
   off += (size_t)L.dstride;                          // second resolved-descriptor buffer
   L.raw0 = (int32_t)off; off += (size_t)c->blob_max * 16;   // single blob landing buffer
