@@ -116,6 +116,7 @@ typedef struct {
   const void* blob;
   const int32_t* blob_off;    /* [n_sites] offset of each site's blob (16-byte units) */
   int32_t blob_max, blob_dtype; /* largest blob (units); dtype the entries were packed for */
+  int32_t max_pairs, pad2;      /* largest chi_l*chi_r of any site */
 } tq_chain;
 
 /* Bytes of device workspace one call needs. */

@@ -255,12 +255,14 @@ def resident_teams(chi: int, d: int = 3) -> int:
     b = 2
     while b < chi:
         b <<= 1
-    slots = 4 + 4 * d if b <= 8 else 2 + 6 * d      # fused small-chi layout vs unfused (gradient sweep)
+    slots = 2 + 3 * d if b <= 8 else 2 + 6 * d      # fused small-chi (direct-G) layout vs unfused (gradient sweep)
     team_bytes = slots * (b + 1) ** 2 * 8 + 4096
     smem = 227 * 1024
     if b <= 8:
-        ctas = max(1, smem // (4 * team_bytes))
-        return int(min(ctas * 4, 64))
+        # 128-thread CTAs; the gradient kernel needs ~128 registers/thread -> at most 4 CTAs/SM
+        # (a 5-CTA register cap was measured slower: more segments add light-cone halo work)
+        ctas = max(1, min(smem // (4 * team_bytes), 4))
+        return int(ctas * 4)
     return int(max(1, min(smem // team_bytes, 2048 // (128 if b == 16 else 256))))
 
 

@@ -61,6 +61,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t raw0, raw1;    // descriptor-blob double buffer
   int32_t dstride;       // bytes between the two resolved-descriptor buffers (mres .. sbuf)
   int32_t sbuf;          // blob header + tq_site copy inside a resolved-descriptor buffer
+  int32_t direct;        // warp teams, one (alpha,beta) pair per lane: G computed in-lane, no G/PIN slots
   int32_t team_bytes;
 };
 
@@ -946,9 +947,13 @@ lr_sweep(Params p) {
     {
       const C* src = env_g + st.env_in;
       const int lper = 2 * lcr;
-      for (int e = tid; e < (npin << lper); e += TEAM) {
-        const int ch = e >> lper, r = e & ((1 << lper) - 1);
-        PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
+      if (!(MODE == 0 && FUSE && p.L.direct)) {
+        for (int e = tid; e < (npin << lper); e += TEAM) {
+          const int ch = e >> lper, r = e & ((1 << lper) - 1);
+          PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
+        }
+      } else if (tid * 32 < (npin << lper)) {
+        asm volatile("prefetch.global.L1 [%0];" :: "l"(src + tid * 32));   // G reads them in-lane later
       }
       const C* ag = env_g + st.a_off;
       const int np = cl * cr;
@@ -995,7 +1000,7 @@ lr_sweep(Params p) {
     }
     if constexpr (MODE == 0) {
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
-      gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
+      if (!(FUSE && p.L.direct)) gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
           [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
           [&](int, int qq) { return PIN + qq * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
@@ -1010,9 +1015,28 @@ lr_sweep(Params p) {
         const int al = tid >> lcr, be = tid & (cr - 1);
         const bool have = tid < cl * cr && !(st.pass_count && !pass_ok(p.c, st, al, be));
         const C z = cmk<C>(R(0), R(0));
+        C g0 = z, g1 = z;
+        if (FUSE && p.L.direct) {
+          // G[s'][al][be] = sum_b sum_k BR[b][s'][al][k] P[b][k][be], P read through L1
+          if (have) {
+            const C* pg = env_g + st.env_in;
+            for (int bb = 0; bb < db; ++bb) {
+              const C* br0 = sm.BR + (bb * 2) * MS + al * LD;
+              const C* br1 = br0 + MS;
+              const C* pb = pg + (size_t)bb * cr * cr + be;
+              for (int k = 0; k < cr; ++k) {
+                const C pv = pb[k * cr];
+                cfma(g0, br0[k], pv);
+                cfma(g1, br1[k], pv);
+              }
+            }
+          }
+        } else if (have) {
+          g0 = G[al * LD + be]; g1 = G[MS + al * LD + be];
+        }
         pair_adjoint_warp<R, 12>(st.op_count, have ? al : 0, have ? be : 0, sm.ocode, sm.ogidx, sm.mres, sm.minfo,
                                  cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
-                                 have ? G[al * LD + be] : z, have ? G[MS + al * LD + be] : z, gpart, tid);
+                                 g0, g1, gpart, tid);
         team_sync<TEAM>();
         STAGE(5);
       } else {
@@ -1305,13 +1329,14 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   const int D = c->d_max < 1 ? 1 : c->d_max;
   size_t off = 0;
   const bool fused = chi <= 8 && D <= 4 && (!lr || mode == 0);   // kernels: FUSE && D <= FDM
+  L.direct = (lr && mode == 0 && fused && team == 32 && c->max_pairs <= 32 && c->max_ops <= 12) ? 1 : 0;
   L.a = (int32_t)off; off += 2 * ms;
   L.ah = L.a;                                        // conjugate transposes are read in place
   L.env = (int32_t)off; off += (size_t)D * ms;       // RL: P in/out; LR: Lambda
-  L.m = (int32_t)off; off += (size_t)(fused ? (lr ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
+  L.m = (int32_t)off; off += (size_t)(fused ? (lr && !L.direct ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
   L.pin = (int32_t)off;
-  if (lr) off += (size_t)D * ms;
+  if (lr && !L.direct) off += (size_t)D * ms;
   L.mr = (int32_t)off;
   if (lr && mode == 1) off += (size_t)2 * D * ms;
   // digit tree (gradient sweep, chi >= 16): per-warp contribution partials; adjoint
