@@ -270,7 +270,7 @@ def run_ours(args, cfg):
     ws_buf, ws_bytes = prog.dp.workspace(batch, _lib.TQ_FLAG_GRAD if cfg.grad else 0, code, stream.cuda_stream)
     energy = torch.empty(batch, 2, dtype=torch.float64, device=dev)
     grad = torch.empty(batch, circuit.n_params, dtype=torch.float32, device=dev) if cfg.grad else None
-    ms_k = (ctypes.c_float * 2)()
+    ms_k = (ctypes.c_float * 3)()
 
     def step(timed=False):
         fn = lib.tq_energy_grad_timed if timed else lib.tq_energy_grad
@@ -303,7 +303,7 @@ def run_ours(args, cfg):
     if sampler:
         sampler.start()
         time.sleep(0.25)
-    step_ms, rl_ms, lr_ms = [], [], []
+    step_ms, rl_ms, lr_ms, adj_ms = [], [], [], []
     barrier()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2); not timed
@@ -315,6 +315,7 @@ def run_ours(args, cfg):
         step_ms.append(e0.elapsed_time(e1))
         rl_ms.append(ms_k[0])
         lr_ms.append(ms_k[1])
+        adj_ms.append(ms_k[2])
     barrier()
     clocks = sampler.stop() if sampler else None
     tot = sum(step_ms)
@@ -371,10 +372,11 @@ def run_ours(args, cfg):
     peak_fp32 = ffma.value
     mean_rl = statistics.mean(rl_ms)
     mean_lr = statistics.mean(lr_ms) if cfg.grad else 0.0
-    if mean_lr >= mean_rl:
-        kname, kms, kflops = "lr_sweep (gradient)", mean_lr, model["flops_lr"] * batch
-    else:
-        kname, kms, kflops = "rl_sweep (energy)", mean_rl, model["flops_rl"] * batch
+    mean_adj = statistics.mean(adj_ms) if cfg.grad else 0.0
+    cands = [("rl_sweep (energy)", mean_rl, model["flops_rl"] * batch),
+             ("lr_sweep (environments + core cotangents)", mean_lr, model["flops_lr"] * batch),
+             ("adj_sweep (column adjoint)", mean_adj, model["flops_adj"] * batch)]
+    kname, kms, kflops = max(cands, key=lambda c: c[1])
     achieved = kflops / (kms * 1e-3) / 1e12
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
@@ -393,7 +395,7 @@ def run_ours(args, cfg):
     if not args.no_cpu_baseline and ws == 1:
         cpu = cpu_baseline_block(cfg, circuit, n, host_cores())
 
-    launches_per_step = 2 + (2 if cfg.grad else 0)  # rl_sweep+reduce_energy (+ lr_sweep+reduce_grad)
+    launches_per_step = 2 + (3 if cfg.grad else 0)  # rl_sweep+reduce_energy (+ lr_sweep+adj_sweep+reduce_grad)
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -404,7 +406,11 @@ def run_ours(args, cfg):
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32 if peak_fp32 else None, "traffic": traffic,
                      "peak_source": "measured FFMA probe (tq_ffma_peak) on this GPU in this run",
                      "flops_per_launch": kflops, "kernel_ms": kms,
-                     "rl_ms": mean_rl, "lr_ms": mean_lr},
+                     "rl_ms": mean_rl, "lr_ms": mean_lr, "adj_ms": mean_adj,
+                     "step_frac": {"rl": mean_rl / ms_per_step, "lr": mean_lr / ms_per_step,
+                                   "adj": mean_adj / ms_per_step},
+                     "all_kernels_frac": (model["flops"] * batch / ((mean_rl + mean_lr + mean_adj) * 1e-3) / 1e12)
+                     / peak_fp32 if peak_fp32 else None},
         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
                 "bytes_per_step": step_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "cpu_baseline": cpu,
@@ -467,12 +473,12 @@ def run_cfg3(args, cfg):
     theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
     m = torch.zeros_like(theta)
     v = torch.zeros_like(theta)
-    ms_k = (ctypes.c_float * 2)()
+    ms_k = (ctypes.c_float * 3)()
     dpe = obj.dp_energy
     ws_buf, ws_bytes = dpe.workspace(B, _lib.TQ_FLAG_GRAD, _lib.TQ_C64, stream.cuda_stream)
     energy = torch.empty(B, 2, dtype=torch.float64, device=dev)
     grad = torch.empty(B, circuit.n_params, dtype=torch.float32, device=dev)
-    kt = {"values": [], "rl": [], "lr": []}
+    kt = {"values": [], "rl": [], "lr": [], "adj": []}
 
     def step(it, timed=False):
         nonlocal theta, m, v
@@ -500,6 +506,7 @@ def run_cfg3(args, cfg):
             kt["values"].append(a.elapsed_time(b))
             kt["rl"].append(ms_k[0])
             kt["lr"].append(ms_k[1])
+            kt["adj"].append(ms_k[2])
 
     for it in range(max(3, args.warmup)):
         step(it)
@@ -549,7 +556,8 @@ def run_cfg3(args, cfg):
     pv = roofline.eval_model(C.compile_chain(circuit, terms, "values", segments=1), grad=True)
     cand = {"values_sweeps (rl+lr values)": (statistics.mean(kt["values"]), (pv["flops_rl"] + pv["flops_lr"]) * B),
             "rl_sweep (cotangent-weighted)": (statistics.mean(kt["rl"]), pe["flops_rl"] * B),
-            "lr_sweep (gradient)": (statistics.mean(kt["lr"]), pe["flops_lr"] * B)}
+            "lr_sweep (gradient)": (statistics.mean(kt["lr"]), pe["flops_lr"] * B),
+            "adj_sweep (column adjoint)": (statistics.mean(kt["adj"]), pe["flops_adj"] * B)}
     kname = max(cand, key=lambda k: cand[k][0])
     kms, kfl = cand[kname]
     achieved = kfl / (kms * 1e-3) / 1e12
@@ -587,7 +595,7 @@ def run_cfg3(args, cfg):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": circuit.n_params * 4,
                 "d2h_bytes_per_step": circuit.n_params * 4 + 8, "note": "single restart through mbe_objective"},
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": 6 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -61,7 +61,8 @@ typedef struct {
   int32_t n_train, ent_begin; /* ent_begin: first of this site's contiguous tq_mat entries */
   int64_t env_in, env_out;  /* complex offsets of the stored right envs at cut k+1 / cut k (-1: none) */
   double init[4];           /* input product-state vector of this qubit (re,im,re,im) */
-  int64_t a_off, pad1;      /* complex offset of the folded core A[2][chi_l][chi_r] (RL stores, LR reloads) */
+  int64_t a_off;            /* complex offset of the folded core A[2][chi_l][chi_r] (RL stores, LR reloads) */
+  int64_t g_off;            /* complex offset of the core cotangent G[2][chi_l][chi_r] (LR stores, adjoint reads) */
 } tq_site;
 
 /* One operator of a column: selects table entry mat + digit (chain.py OP_DTYPE).
@@ -111,7 +112,7 @@ typedef struct {
   const int32_t* gred_idx;
   const int32_t* term_active; /* [n_terms] 0 for identity terms (value 1) */
   /* Per-site descriptor blobs (16-byte units), prefetched with cp.async one site ahead:
-   * [header {len, next_rl, next_lr, 0}] [tq_site: 9 units] [ops: {opcode, gidx, tbase, tidx}]
+   * [header {len, next_rl, next_lr, segment}] [tq_site: 9 units] [ops: {opcode, gidx, tbase, tidx}]
    * [factor entries: complex64 3 units / complex128 6 units] [rl edges] [lr edges]. */
   const void* blob;
   const int32_t* blob_off;    /* [n_sites] offset of each site's blob (16-byte units) */
@@ -142,8 +143,9 @@ tq_status tq_inner(const tq_chain* bra, const void* theta_bra, int64_t bra_strid
                    const tq_chain* ket, const void* theta_ket, int64_t ket_stride,
                    int32_t dtype, int32_t batch, double* out, void* stream);
 
-/* tq_energy_grad with CUDA events around the two sweep kernels on `stream` (synchronises);
- * ms_out[0] = right-to-left sweep, ms_out[1] = left-to-right gradient sweep.  Bench/diagnostic. */
+/* tq_energy_grad with CUDA events around the kernels on `stream` (synchronises);
+ * ms_out[0] = right-to-left sweep, ms_out[1] = left-to-right sweep, ms_out[2] = column
+ * adjoint (adj_sweep).  Bench/diagnostic. */
 tq_status tq_energy_grad_timed(const tq_chain* chain, int32_t dtype, int32_t batch,
                                const void* theta, int64_t theta_stride,
                                const void* coef, int64_t coef_stride,

@@ -142,12 +142,14 @@ def build_blobs(plan: C.ChainPlan, dtype_code: int):
     total = int(lens.sum()) if nsite else 1
     bmax = int(lens.max()) if nsite else 1
     buf = np.zeros((total + bmax) * 16, dtype=np.uint8)   # tail padding: prefetches copy bmax units
+    seg_of = np.zeros(nsite, dtype=np.int64)
     nxt_rl = np.full(nsite, -1, dtype=np.int64)
     nxt_lr = np.full(nsite, -1, dtype=np.int64)
-    for sg in plan.segs:
+    for si, sg in enumerate(plan.segs):
         b0, cnt = int(sg["site_begin"]), int(sg["site_count"])
         for k in range(cnt):
             i = b0 + k
+            seg_of[i] = si
             if k > 0:
                 nxt_rl[i] = offs[i - 1]
             if k + 1 < cnt:
@@ -156,7 +158,7 @@ def build_blobs(plan: C.ChainPlan, dtype_code: int):
     for i in range(nsite):
         st = sites[i]
         base = int(offs[i]) * 16
-        hdr = np.array([lens[i], nxt_rl[i], nxt_lr[i], 0], dtype=np.int32)
+        hdr = np.array([lens[i], nxt_rl[i], nxt_lr[i], seg_of[i]], dtype=np.int32)
         buf[base:base + 16] = hdr.view(np.uint8)
         buf[base + 16:base + 16 + 16 * SITE_UNITS] = np.frombuffer(st.tobytes(), dtype=np.uint8)
         o = base + 16 + 16 * SITE_UNITS

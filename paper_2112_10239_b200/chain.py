@@ -46,7 +46,7 @@ SITE_DTYPE = np.dtype([
     ("n_train", "<i4"), ("ent_begin", "<i4"),
     ("env_in", "<i8"), ("env_out", "<i8"),
     ("init", "<f8", (4,)),
-    ("a_off", "<i8"), ("pad1", "<i8"),
+    ("a_off", "<i8"), ("g_off", "<i8"),
 ], align=True)
 OP_DTYPE = np.dtype([("mat", "<i4"), ("lmat", "<i4"), ("src", "<i4"), ("shift", "<i4"), ("bits", "<i4"),
                      ("tidx", "<i4"), ("gidx", "<i4"), ("toff", "<i4"), ("tbase", "<i4"), ("pad", "<i4")],
@@ -439,6 +439,11 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         for q in range(nsite):
             a_off[q] = off
             off += 2 * int(chis_cut[q]) * int(chis_cut[q + 1])
+        g_off = np.zeros(nsite, dtype=np.int64)      # core cotangents G_k[s], LR sweep -> adjoint kernel
+        if mode == "energy":
+            for q in range(nsite):
+                g_off[q] = off
+                off += 2 * int(chis_cut[q]) * int(chis_cut[q + 1])
         seg_env = off
 
         # ---- emit site records
@@ -496,6 +501,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
             rec["lr_da"], rec["lr_db"] = len(lr_ch[q]), len(lr_ch[q + 1])
             rec["env_in"], rec["env_out"] = env_off[q + 1], env_off[q]
             rec["a_off"] = a_off[q]
+            rec["g_off"] = g_off[q]
             v = np.array([1, 0], dtype=complex) if init_vecs is None else init_vecs[c_lo + q]
             rec["init"] = [v[0].real, v[0].imag, v[1].real, v[1].imag]
             sites.append(rec)

@@ -218,7 +218,7 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
     minfo[e] = ip[0];
     mps[e] = rp[FO];
   }
-  const int ec = rl ? st.rl_edge_count : st.lr_edge_count;
+  const int ec = sedge ? (rl ? st.rl_edge_count : st.lr_edge_count) : 0;
   for (int ei = tid; ei < ec; ei += TEAM) {
     const int4 r = edg[ei];
     SEdge<R> se; se.a = r.x; se.b = r.y; se.op = r.z; se.coef = r.w < 0 ? R(1) : coef_row[r.w];
@@ -916,8 +916,8 @@ lr_sweep(Params p) {
   STAGE_BEGIN();
 
   const tq_segment seg = p.c.segs[g];
-  const C* env_g = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
-  R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
+  C* env_g_w = reinterpret_cast<C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base;
+  const C* env_g = env_g_w;
   if (tid == 0) LAM[0] = cmk<C>(R(1), R(0));
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
   int4* const raw0 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0);
@@ -1006,138 +1006,34 @@ lr_sweep(Params p) {
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(4);
-      // ---- column adjoint: per (alpha, beta) pair forward fold keeping the components
-      // projectors discard, then the backward walk accumulating Im<u, sigma v>.
-      const int ntr = st.n_train;
-      R* contrib = sm.contrib;
-      if (TEAM == 32 && CHI <= 8 && cl * cr <= 32 && st.op_count <= 12) {
-        // one (alpha, beta) pair per lane: warp-direct adjoint + reduction
-        const int al = tid >> lcr, be = tid & (cr - 1);
-        const bool have = tid < cl * cr && !(st.pass_count && !pass_ok(p.c, st, al, be));
-        const C z = cmk<C>(R(0), R(0));
-        C g0 = z, g1 = z;
-        if (FUSE && p.L.direct) {
-          // G[s'][al][be] = sum_b sum_k BR[b][s'][al][k] P[b][k][be], P read through L1
-          if (have) {
-            const C* pg = env_g + st.env_in;
-            for (int bb = 0; bb < db; ++bb) {
-              const C* br0 = sm.BR + (bb * 2) * MS + al * LD;
-              const C* br1 = br0 + MS;
-              const C* pb = pg + (size_t)bb * cr * cr + be;
-              for (int k = 0; k < cr; ++k) {
-                const C pv = pb[k * cr];
-                cfma(g0, br0[k], pv);
-                cfma(g1, br1[k], pv);
-              }
+      // ---- core cotangent G_k -> HBM; the column adjoint runs in adj_sweep (off the critical path)
+      C* gg = env_g_w + st.g_off;
+      const int np = cl * cr;
+      if (FUSE && p.L.direct) {
+        // G[s'][al][be] = sum_b sum_k BR[b][s'][al][k] P[b][k][be], one pair per lane, P through L1
+        if (tid < np) {
+          const int al = tid >> lcr, be = tid & (cr - 1);
+          C g0 = cmk<C>(R(0), R(0)), g1 = g0;
+          const C* pg = env_g + st.env_in;
+          for (int bb = 0; bb < db; ++bb) {
+            const C* br0 = sm.BR + (bb * 2) * MS + al * LD;
+            const C* br1 = br0 + MS;
+            const C* pb = pg + (size_t)bb * cr * cr + be;
+            for (int k = 0; k < cr; ++k) {
+              const C pv = pb[k * cr];
+              cfma(g0, br0[k], pv);
+              cfma(g1, br1[k], pv);
             }
           }
-        } else if (have) {
-          g0 = G[al * LD + be]; g1 = G[MS + al * LD + be];
+          gg[tid] = g0; gg[np + tid] = g1;
         }
-        pair_adjoint_warp<R, 12>(st.op_count, have ? al : 0, have ? be : 0, sm.ocode, sm.ogidx, sm.mres, sm.minfo,
-                                 cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
-                                 g0, g1, gpart, tid);
-        team_sync<TEAM>();
-        STAGE(5);
       } else {
-      const int cw = p.L.tree ? TEAM / 32 : TEAM;      // contribution columns: warps (tree) or threads
-      if (tid < cw) for (int t = 0; t < ntr; ++t) contrib[t * cw + tid] = R(0);
-      const int npair = p.L.tree ? 0 : cl * cr;
-      const bool one_pair = npair <= TEAM;
-      const int nops = st.op_count;
-      if constexpr (CHI >= 16) {
-        if (p.L.tree) {
-          team_sync<TEAM>();                          // contrib zeroed before per-warp accumulation
-          tree_forward<R, TEAM>(st, tid, sm.mres, sm.ocode, sm.obase, sm.lev);
-          tree_adjoint<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.minfo, sm.ocode, sm.obase, sm.lev, sm.ubuf, G, contrib);
+        for (int e = tid; e < 2 * np; e += TEAM) {
+          const int sidx = e >= np, r = e - sidx * np;
+          gg[e] = G[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))];
         }
       }
-      for (int pi = tid; pi < npair; pi += TEAM) {
-        const int al = pi >> lcr, be = pi & (cr - 1);
-        if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
-        C sv[MAXSAVE];
-        int ns = 0;
-        C v0 = cmk<C>(R(st.init[0]), R(st.init[1]));
-        C v1 = cmk<C>(R(st.init[2]), R(st.init[3]));
-        for (int oi = 0; oi < nops; ++oi) {
-          const int c = sm.ocode[oi];
-          const int e = oc_lmat(c) + oc_digit(c, al, be);
-          const int cls = (sm.minfo[e] >> 8) & 0xff;
-          if (cls == 1) sv[ns++] = v1;
-          else if (cls == 2) sv[ns++] = v0;
-          else if (cls == 3) { sv[ns++] = v0; sv[ns++] = v1; }
-          const C* Mm = sm.mres + 4 * e;
-          C n0 = cmul(Mm[0], v0); cfma(n0, Mm[1], v1);
-          C n1 = cmul(Mm[2], v0); cfma(n1, Mm[3], v1);
-          v0 = n0; v1 = n1;
-        }
-        C u0 = G[al * LD + be], u1 = G[MS + al * LD + be];
-        for (int oi = nops - 1; oi >= 0; --oi) {
-          const int c = sm.ocode[oi];
-          const int e = oc_lmat(c) + oc_digit(c, al, be);
-          const int info = sm.minfo[e];
-          const int kind = info & 0xff, cls = (info >> 8) & 0xff;
-          const int tix = oc_tidx(c);
-          if (tix >= 0 && kind != 0) {
-            // Im<u, sigma v>, sigma = X (kind 1), Y (2), Z (3)
-            C s0, s1;
-            if (kind == 1) { s0 = v1; s1 = v0; }
-            else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
-            else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
-            C d = cmk<C>(R(0), R(0));
-            cfmac(d, u0, s0); cfmac(d, u1, s1);
-            if (one_pair) contrib[tix * TEAM + tid] = d.y;
-            else contrib[tix * TEAM + tid] += d.y;
-          }
-          const C* Mm = sm.mres + 4 * e;
-          C w0 = cmk<C>(R(0), R(0)), w1 = w0;   // u <- M^H u
-          cfmac(w0, Mm[0], u0); cfmac(w0, Mm[2], u1);
-          cfmac(w1, Mm[1], u0); cfmac(w1, Mm[3], u1);
-          u0 = w0; u1 = w1;
-          if (cls == 0) {                        // v <- state before this op
-            C x0 = cmk<C>(R(0), R(0)), x1 = x0;
-            cfmac(x0, Mm[0], v0); cfmac(x0, Mm[2], v1);
-            cfmac(x1, Mm[1], v0); cfmac(x1, Mm[3], v1);
-            v0 = x0; v1 = x1;
-          } else if (cls == 1) {
-            const R sc = sm.mps[e];
-            v0 = cmk<C>(v0.x * sc, v0.y * sc); v1 = sv[--ns];
-          } else if (cls == 2) {
-            const R sc = sm.mps[e];
-            v1 = cmk<C>(v1.x * sc, v1.y * sc); v0 = sv[--ns];
-          } else {
-            v1 = sv[--ns]; v0 = sv[--ns];
-          }
-        }
-      }
-      team_sync<TEAM>();
       STAGE(5);
-      // deterministic reduction, four trainable ops per warp pass: strided lane sums then an
-      // xor tree; lane 0 writes the op's partial gradient slot
-      {
-        const int warp = tid >> 5, lane = tid & 31;
-        constexpr int NW = TEAM / 32;
-        for (int t0 = warp * 4; t0 < ntr; t0 += NW * 4) {
-          R sacc[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            sacc[u] = R(0);
-            if (t0 + u < ntr)
-              for (int k = lane; k < cw; k += 32) sacc[u] += contrib[(t0 + u) * cw + k];
-          }
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], off);
-          if (lane == 0)
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (t0 + u < ntr) gpart[sm.ogidx[t0 + u]] = sacc[u];
-        }
-      }
-      team_sync<TEAM>();
-      STAGE(6);
-      }   // per-pair / tree adjoint
     } else {
       // ---- values: rho_a[s'][s] = <A[s'], M[a][s] R> for every source channel a
       gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cr, 1,
@@ -1194,6 +1090,165 @@ lr_sweep(Params p) {
   STAGE_END(1);
 }
 
+
+
+// ------------------------------------------------------------------ column adjoint kernel
+// One team per (theta-set, site): resolves the site's descriptors, reads the core cotangent
+// G_k written by lr_sweep and pushes it through the column to the site's trainable angles.
+// Every (theta-set, site) is independent, so this runs at full occupancy instead of on
+// the left-to-right sweep's sequential critical path.
+struct AdjLayout {
+  int32_t g, mres, minfo, mps, ocode, ogidx, obase, sbuf, raw, lev, ubuf, contrib, team_bytes, tree;
+};
+
+template <typename R, int CHI, int TEAM>
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
+adj_sweep(Params p, AdjLayout A) {
+  using C = typename CT<R>::T;
+  constexpr int LD = CHI + 1;
+  constexpr int MS = LD * LD;
+  constexpr int TEAMS = TEAM == 32 ? 4 : 1;
+  constexpr int MAXSAVE = 48;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int team = threadIdx.x / TEAM;
+  const int tid = threadIdx.x % TEAM;
+  const int nsites = p.c.n_sites;
+  const int unit = blockIdx.x * TEAMS + team;
+  if (unit >= p.batch * nsites) return;
+  const int b = unit / nsites, si = unit % nsites;
+  unsigned char* base = smem_raw + (size_t)team * A.team_bytes;
+  C* Gs = reinterpret_cast<C*>(base + A.g);
+  C* mres = reinterpret_cast<C*>(base + A.mres);
+  int* minfo = reinterpret_cast<int*>(base + A.minfo);
+  R* mps = reinterpret_cast<R*>(base + A.mps);
+  int* ocode = reinterpret_cast<int*>(base + A.ocode);
+  int* ogidx = reinterpret_cast<int*>(base + A.ogidx);
+  int* obase = reinterpret_cast<int*>(base + A.obase);
+  int4* sbuf = reinterpret_cast<int4*>(base + A.sbuf);
+  int4* raw = reinterpret_cast<int4*>(base + A.raw);
+  const int4* blob = reinterpret_cast<const int4*>(p.c.blob) + p.c.blob_off[si];
+  for (int c = tid; c < p.c.blob_max; c += TEAM) raw[c] = blob[c];
+  team_sync<TEAM>();
+  const tq_site st = *reinterpret_cast<const tq_site*>(raw + 1);
+  if (st.n_train == 0) return;   // uniform across the team
+  const int g = raw[0].w;
+  const tq_segment seg = p.c.segs[g];
+  const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
+  const C* gg = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base + st.g_off;
+  R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
+  stage_blob<R, TEAM>(raw, st, theta_b, nullptr, true, tid, mres, minfo, mps, ocode, ogidx, obase, nullptr, sbuf);
+  const int cl = st.chi_l, cr = st.chi_r;
+  const int lcr = 31 - __clz(cr);
+  const int np = cl * cr;
+  const int nops = st.op_count;
+  if (TEAM == 32 && CHI <= 8 && np <= 32 && nops <= 12) {
+    team_sync<TEAM>();
+    const int al = tid >> lcr, be = tid & (cr - 1);
+    const bool have = tid < np && !(st.pass_count && !pass_ok(p.c, st, al, be));
+    const C z = cmk<C>(R(0), R(0));
+    pair_adjoint_warp<R, 12>(nops, have ? al : 0, have ? be : 0, ocode, ogidx, mres, minfo,
+                             cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
+                             have ? gg[tid] : z, have ? gg[np + tid] : z, gpart, tid);
+    return;
+  }
+  for (int e = tid; e < 2 * np; e += TEAM) {
+    const int sidx = e >= np, r = e - sidx * np;
+    Gs[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))] = gg[e];
+  }
+  const int ntr = st.n_train;
+  R* contrib = reinterpret_cast<R*>(base + A.contrib);
+  const int cw = A.tree ? TEAM / 32 : TEAM;
+  if (tid < cw) for (int t = 0; t < ntr; ++t) contrib[t * cw + tid] = R(0);
+  team_sync<TEAM>();
+  if constexpr (CHI >= 16) {
+    if (A.tree) {
+      C* lev = reinterpret_cast<C*>(base + A.lev);
+      C* ubuf = reinterpret_cast<C*>(base + A.ubuf);
+      tree_forward<R, TEAM>(st, tid, mres, ocode, obase, lev);
+      tree_adjoint<R, LD, TEAM>(p.c, st, tid, mres, minfo, ocode, obase, lev, ubuf, Gs, contrib);
+    }
+  }
+  const bool one_pair = np <= TEAM;
+  for (int pi = tid; !A.tree && pi < np; pi += TEAM) {
+    const int al = pi >> lcr, be = pi & (cr - 1);
+    if (st.pass_count && !pass_ok(p.c, st, al, be)) continue;
+    C sv[MAXSAVE];
+    int ns = 0;
+    C v0 = cmk<C>(R(st.init[0]), R(st.init[1]));
+    C v1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+    for (int oi = 0; oi < nops; ++oi) {
+      const int c = ocode[oi];
+      const int e = oc_lmat(c) + oc_digit(c, al, be);
+      const int cls = (minfo[e] >> 8) & 0xff;
+      if (cls == 1) sv[ns++] = v1;
+      else if (cls == 2) sv[ns++] = v0;
+      else if (cls == 3) { sv[ns++] = v0; sv[ns++] = v1; }
+      const C* Mm = mres + 4 * e;
+      C n0 = cmul(Mm[0], v0); cfma(n0, Mm[1], v1);
+      C n1 = cmul(Mm[2], v0); cfma(n1, Mm[3], v1);
+      v0 = n0; v1 = n1;
+    }
+    C u0 = Gs[al * LD + be], u1 = Gs[MS + al * LD + be];
+    for (int oi = nops - 1; oi >= 0; --oi) {
+      const int c = ocode[oi];
+      const int e = oc_lmat(c) + oc_digit(c, al, be);
+      const int info = minfo[e];
+      const int kind = info & 0xff, cls = (info >> 8) & 0xff;
+      const int tix = oc_tidx(c);
+      if (tix >= 0 && kind != 0) {
+        C s0, s1;
+        if (kind == 1) { s0 = v1; s1 = v0; }
+        else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
+        else { s0 = v0; s1 = cmk<C>(-v1.x, -v1.y); }
+        C d = cmk<C>(R(0), R(0));
+        cfmac(d, u0, s0); cfmac(d, u1, s1);
+        if (one_pair) contrib[tix * TEAM + tid] = d.y;
+        else contrib[tix * TEAM + tid] += d.y;
+      }
+      const C* Mm = mres + 4 * e;
+      C w0 = cmk<C>(R(0), R(0)), w1 = w0;
+      cfmac(w0, Mm[0], u0); cfmac(w0, Mm[2], u1);
+      cfmac(w1, Mm[1], u0); cfmac(w1, Mm[3], u1);
+      u0 = w0; u1 = w1;
+      if (cls == 0) {
+        C x0 = cmk<C>(R(0), R(0)), x1 = x0;
+        cfmac(x0, Mm[0], v0); cfmac(x0, Mm[2], v1);
+        cfmac(x1, Mm[1], v0); cfmac(x1, Mm[3], v1);
+        v0 = x0; v1 = x1;
+      } else if (cls == 1) {
+        const R sc = mps[e];
+        v0 = cmk<C>(v0.x * sc, v0.y * sc); v1 = sv[--ns];
+      } else if (cls == 2) {
+        const R sc = mps[e];
+        v1 = cmk<C>(v1.x * sc, v1.y * sc); v0 = sv[--ns];
+      } else {
+        v1 = sv[--ns]; v0 = sv[--ns];
+      }
+    }
+  }
+  team_sync<TEAM>();
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    constexpr int NW = TEAM / 32;
+    for (int t0 = warp * 4; t0 < ntr; t0 += NW * 4) {
+      R sacc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sacc[u] = R(0);
+        if (t0 + u < ntr)
+          for (int k = lane; k < cw; k += 32) sacc[u] += contrib[(t0 + u) * cw + k];
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], off);
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t0 + u < ntr) gpart[ogidx[t0 + u]] = sacc[u];
+    }
+  }
+}
 
 // ------------------------------------------------------------------ inner product sweep
 // out[b] = <bra(theta_bra_b) | ket(theta_ket_b)>: one left-to-right transfer with distinct
@@ -1343,8 +1398,8 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   // ping-pong buffers in the M slots after G (free during the adjoint); levels dedicated
   // when they fit (then the fold builds them and the adjoint reuses them), else in scratch.
   const int ntr = c->max_train > 0 ? c->max_train : 1;
-  const bool want_tree = lr && mode == 0 && chi >= 16 && (size_t)chi * chi <= (size_t)4 * team;  // EPT entries/thread
-  size_t need = lr ? (size_t)(mode == 0 ? ntr : 8 * D) * (want_tree ? team / 32 : team) * rsz : 0;
+  const bool want_tree = false;   // the column adjoint lives in adj_sweep
+  size_t need = (lr && mode == 1) ? (size_t)8 * D * team * rsz : 0;
   if (need <= (size_t)2 * D * ms && !want_tree) L.contrib = L.br;
   else { L.contrib = (int32_t)off; off += align_up(need, 16); }
   off = align_up(off, 16);
@@ -1393,8 +1448,38 @@ static WsLayout ws_layout(const tq_chain* c, int batch, int flags, int dtype) {
   return w;
 }
 
-struct Timing { cudaEvent_t ev[4]; bool on; };
-static thread_local Timing g_timing = {{nullptr, nullptr, nullptr, nullptr}, false};
+struct Timing { cudaEvent_t ev[6]; bool on; };
+static thread_local Timing g_timing = {{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}, false};
+
+static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rsz) {
+  AdjLayout A{};
+  const size_t csz = 2 * rsz;
+  const size_t ms = (size_t)(chi + 1) * (chi + 1) * csz;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const int32_t o = (int32_t)off; off = align_up(off + bytes, 16); return o; };
+  A.g = take(2 * ms);
+  A.mres = take((size_t)c->max_lmat * 4 * csz);
+  A.minfo = take((size_t)c->max_lmat * 4);
+  A.mps = take((size_t)c->max_lmat * rsz);
+  const size_t nops = (size_t)(c->max_ops > 0 ? c->max_ops : 1);
+  A.ocode = take(nops * 4); A.ogidx = take(nops * 4); A.obase = take(nops * 4);
+  A.sbuf = take(16 + sizeof(tq_site));
+  A.raw = take((size_t)c->blob_max * 16);
+  const int ntr = c->max_train > 0 ? c->max_train : 1;
+  const size_t budget = (size_t)227 * 1024 / (team == 32 ? 4 : 1);
+  A.tree = 0;
+  if (chi >= 16) {
+    const size_t lev = (size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz;
+    const size_t ub = (size_t)2 * chi * chi * 2 * csz;
+    const size_t ctb = (size_t)ntr * (team / 32) * rsz;
+    if (align_up(off + lev + ub + ctb + 64, 128) <= budget) {
+      A.tree = 1; A.lev = take(lev); A.ubuf = take(ub); A.contrib = take(ctb);
+    }
+  }
+  if (!A.tree) A.contrib = take((size_t)ntr * team * rsz);
+  A.team_bytes = (int32_t)align_up(off, 128);
+  return A;
+}
 
 template <typename R, int CHI, bool FUSED>
 static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
@@ -1430,6 +1515,18 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     if (g_timing.on) cudaEventRecord(g_timing.ev[3], s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
+    if (prm.mode == 0) {
+      AdjLayout A = make_adj_layout(&prm.c, CHI, TEAM, sizeof(R));
+      const size_t asmem = (size_t)A.team_bytes * TEAMS;
+      if (asmem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "adjoint shared-memory layout exceeds 227 KB");
+      const int64_t units = (int64_t)prm.batch * prm.c.n_sites;
+      cudaFuncSetAttribute(adj_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem);
+      if (g_timing.on) cudaEventRecord(g_timing.ev[4], s);
+      adj_sweep<R, CHI, TEAM><<<(unsigned)((units + TEAMS - 1) / TEAMS), TEAM * TEAMS, asmem, s>>>(prm, A);
+      if (g_timing.on) cudaEventRecord(g_timing.ev[5], s);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
+    }
   }
   return TQ_OK;
 }
@@ -1595,19 +1692,19 @@ tq_status tq_term_values(const tq_chain* chain, int32_t dtype, int32_t batch, co
 tq_status tq_energy_grad_timed(const tq_chain* chain, int32_t dtype, int32_t batch, const void* theta,
                                int64_t theta_stride, const void* coef, int64_t coef_stride, double* energy, void* grad,
                                void* workspace, size_t workspace_bytes, void* stream, float* ms_out) {
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&g_timing.ev[i]);
+  for (int i = 0; i < 6; ++i) cudaEventCreate(&g_timing.ev[i]);
   g_timing.on = true;
   tq_status st = tq_energy_grad(chain, dtype, batch, theta, theta_stride, coef, coef_stride, energy, grad, workspace,
                                 workspace_bytes, stream);
   g_timing.on = false;
   if (st == TQ_OK) {
-    cudaEventSynchronize(g_timing.ev[grad ? 3 : 1]);
-    float a = 0.f, b = 0.f;
+    cudaEventSynchronize(g_timing.ev[grad ? 5 : 1]);
+    float a = 0.f, b = 0.f, c2 = 0.f;
     cudaEventElapsedTime(&a, g_timing.ev[0], g_timing.ev[1]);
-    if (grad) cudaEventElapsedTime(&b, g_timing.ev[2], g_timing.ev[3]);
-    ms_out[0] = a; ms_out[1] = b;
+    if (grad) { cudaEventElapsedTime(&b, g_timing.ev[2], g_timing.ev[3]); cudaEventElapsedTime(&c2, g_timing.ev[4], g_timing.ev[5]); }
+    ms_out[0] = a; ms_out[1] = b; ms_out[2] = c2;
   }
-  for (int i = 0; i < 4; ++i) cudaEventDestroy(g_timing.ev[i]);
+  for (int i = 0; i < 6; ++i) cudaEventDestroy(g_timing.ev[i]);
   return st;
 }
 
@@ -1681,7 +1778,7 @@ int32_t tq_stage_cycles(unsigned long long* out) {
 #endif
 
 const char* tq_build_info(void) {
-  return "tq_engine sm_100a: rl_sweep/lr_sweep<float|double, chi 2..32>, reduce_energy, reduce_grad, inner_sweep, ffma_probe";
+  return "tq_engine sm_100a: rl_sweep/lr_sweep<float|double, chi 2..32>, adj_sweep, reduce_energy, reduce_grad, inner_sweep, ffma_probe";
 }
 
 }  // extern "C"

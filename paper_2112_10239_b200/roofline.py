@@ -36,8 +36,19 @@ def sweep_cmacs(plan) -> dict:
               + 4 * s["lr_da"] * cl * cr * (s["fin_count"] > 0) + 2 * s["lr_edge_count"] * cl * cr)
         adj = np.zeros_like(fold)
     else:
-        adj = pairs * nops * 12
-    return {"rl": float(np.sum(fold + rl)), "lr": float(np.sum(fold + lr + adj)),
+        # column adjoint counted on the digit tree (the minimal walk): per tree entry one
+        # forward matvec (4), one backward matvec (4), the digit reduction (~2) and the
+        # sigma contraction (2)
+        ops = plan.ops
+        adj = np.zeros_like(fold)
+        for i in range(len(s)):
+            b, c = int(s["op_begin"][i]), int(s["op_count"][i])
+            if c:
+                last = ops[b + c - 1]
+                entries = int(last["tbase"]) + (1 << (int(last["toff"]) + int(last["bits"])))
+                adj[i] = 12.0 * entries
+    # the left-to-right sweep reloads the folded cores stored by the right-to-left sweep
+    return {"rl": float(np.sum(fold + rl)), "lr": float(np.sum(lr)), "adj": float(np.sum(adj)),
             "fold": float(np.sum(fold)), "adjoint": float(np.sum(adj))}
 
 
@@ -51,9 +62,10 @@ def eval_model(plan, grad: bool = True, real_bytes: int = 4) -> dict:
     c = sweep_cmacs(plan)
     flops_rl = 8 * c["rl"]
     flops_lr = 8 * c["lr"] if grad else 0.0
+    flops_adj = 8 * c["adj"] if grad else 0.0
     P = plan.n_params
     byts = P * real_bytes + 16
     if grad:
         byts += P * real_bytes + 2 * env_bytes(plan, real_bytes)
-    return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops": flops_rl + flops_lr, "bytes": byts,
-            "cmacs": c}
+    return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops_adj": flops_adj,
+            "flops": flops_rl + flops_lr + flops_adj, "bytes": byts, "cmacs": c}

@@ -39,7 +39,7 @@ items = B * plan.n_segments
 sites = B * int(plan.info["sub_chain_sites"])
 print(f"{name} B={B} segments={plan.n_segments} sub-chain sites={plan.info['sub_chain_sites']} chi={plan.chi_max}")
 rl = ["stage", "fold", "N gemm", "bracket", "P gemm"]
-lr = ["stage+PIN", "fold", "M gemm", "bracket", "Lam+G gemm", "adjoint", "reduce", "values MR", "values dots", "values fin"]
+lr = ["stage+PIN+A", "-", "M gemm", "bracket", "Lam+G gemm", "G store", "-", "values MR", "values dots", "values fin"]
 for k, names in ((0, rl), (1, lr)):
     tot = sum(buf[16 * k + i] for i in range(16))
     if not tot:
