@@ -188,3 +188,34 @@ def with_params(circuit: Circuit, theta) -> Circuit:
         g = gates[idx]
         gates[idx] = standard_gate(g.name, g.wires, float(theta[slot]))
     return Circuit(circuit.n_qubits, tuple(gates), circuit.trainable)
+
+
+# ---------------------------------------------------------------- JSON documents
+# Same document shape as the reference (circuits.py:344-372), so circuit files written by
+# ``tnsim`` load here unchanged and vice versa: {"n_qubits", "gates": [{name, wires[, param]}],
+# "trainable": [...]}.
+
+def circuit_to_dict(circuit: Circuit) -> dict:
+    out_gates = []
+    for g in circuit.gates:
+        if g.name not in STANDARD_GATES:
+            raise UnknownGate(f"gate '{g.name}' has no JSON form (custom matrix)")
+        doc = {"name": g.name, "wires": list(g.wires)}
+        if g.param is not None:
+            doc["param"] = g.param
+        out_gates.append(doc)
+    return {"n_qubits": circuit.n_qubits, "gates": out_gates, "trainable": list(circuit.trainable)}
+
+
+def circuit_from_dict(doc: dict) -> Circuit:
+    """Inverse of :func:`circuit_to_dict`; structural problems raise ``ParseError``."""
+    from .errors import ParseError
+
+    try:
+        n = int(doc["n_qubits"])
+        entries = doc["gates"]
+        trainable = tuple(int(i) for i in doc.get("trainable", ()))
+        gates = tuple(standard_gate(e["name"], e["wires"], e.get("param")) for e in entries)
+    except (KeyError, TypeError) as exc:
+        raise ParseError(f"malformed circuit document: {exc!r}") from exc
+    return Circuit(n, gates, trainable)

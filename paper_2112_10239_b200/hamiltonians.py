@@ -92,3 +92,50 @@ def tfim(n_qubits: int, j: float = 1.0, h: float = 1.0, periodic: bool = False) 
     terms = [term(-float(j), {k: "Z", (k + 1) % n: "Z"}) for k in range(bonds)]
     terms += [term(-float(h), {k: "X"}) for k in range(n)]
     return PauliHamiltonian(n, tuple(terms))
+
+
+# ---------------------------------------------------------------- JSON documents
+# Reference document shape (hamiltonians.py:227-271): {"n_qubits", "terms": [{"coeff": real,
+# "ops": {"<qubit>": "X"|"Y"|"Z"}}]}.
+
+def hamiltonian_to_dict(ham: PauliHamiltonian) -> dict:
+    return {"n_qubits": ham.n_qubits,
+            "terms": [{"coeff": t.coeff.real, "ops": {str(q): op for q, op in t.ops}} for t in ham.terms]}
+
+
+def hamiltonian_from_dict(doc) -> PauliHamiltonian:
+    """Validating loader; every structural problem is a ``ParseError`` (an ``InputError``)."""
+    from .errors import ParseError
+
+    if not isinstance(doc, dict):
+        raise ParseError(f"expected an object, got {type(doc).__name__}")
+    try:
+        n = int(doc["n_qubits"])
+        entries = doc["terms"]
+    except (KeyError, TypeError, ValueError) as exc:
+        raise ParseError(f"malformed Hamiltonian object: {exc}") from exc
+    if not isinstance(entries, list):
+        raise ParseError("'terms' must be a list")
+    out = []
+    for i, e in enumerate(entries):
+        if not isinstance(e, dict) or "coeff" not in e or "ops" not in e:
+            raise ParseError(f"term {i} must have 'coeff' and 'ops'")
+        c = e["coeff"]
+        if isinstance(c, bool) or not isinstance(c, (int, float)):
+            raise ParseError(f"term {i} coefficient must be a real number")
+        if not isinstance(e["ops"], dict):
+            raise ParseError(f"term {i} 'ops' must be an object")
+        ops = {}
+        for key, letter in e["ops"].items():
+            try:
+                ops[int(key)] = letter
+            except (TypeError, ValueError):
+                raise ParseError(f"term {i} has non-integer qubit key {key!r}")
+        try:
+            out.append(term(float(c), ops))
+        except InputError as exc:
+            raise ParseError(f"term {i}: {exc}") from exc
+    try:
+        return PauliHamiltonian(n, tuple(out))
+    except InputError as exc:
+        raise ParseError(str(exc)) from exc
