@@ -23,6 +23,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "../../include/tq_engine.h"
 
 namespace tq {
@@ -61,7 +63,9 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t raw0, raw1;    // descriptor-blob double buffer
   int32_t dstride;       // bytes between the two resolved-descriptor buffers (mres .. sbuf)
   int32_t sbuf;          // blob header + tq_site copy inside a resolved-descriptor buffer
-  int32_t direct;        // warp teams, one (alpha,beta) pair per lane: G computed in-lane, no G/PIN slots
+  int32_t direct;        // warp teams, one (alpha,beta) pair per lane: G computed in-lane, no G slots;
+                         // folded cores (A, A2 ping-pong) and P (dense) are cp.async-prefetched
+  int32_t a2;            // second folded-core buffer (direct path)
   int32_t team_bytes;
 };
 
@@ -170,12 +174,38 @@ static_assert(sizeof(tq_site) % 16 == 0, "tq_site must be a multiple of 16 bytes
 // One site's descriptors live in a contiguous 16-byte-aligned blob (include/tq_engine.h);
 // the sweeps copy the NEXT site's blob into a shared-memory double buffer with cp.async
 // while the current site computes, so descriptor staging never waits on global memory.
-__device__ __forceinline__ void blob_prefetch(int4* dst, const int4* src, int units, int tid, int team) {
+__device__ __forceinline__ void async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void blob_prefetch(int4* dst, const int4* src, int units, int tid, int team,
+                                              bool commit = true) {
   for (int c = tid; c < units; c += team) {
     const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(saddr), "l"(src + c) : "memory");
   }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  if (commit) async_commit();
+}
+// one complex element global -> shared, asynchronously (8 or 16 bytes)
+template <typename C>
+__device__ __forceinline__ void async_elem(C* dst, const C* src) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if constexpr (sizeof(C) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(saddr), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(saddr), "l"(src) : "memory");
+}
+// folded core [2][cl][cr] (dense, HBM) -> padded LD layout in shared memory
+template <typename C, int LD, int TEAM>
+__device__ __forceinline__ void async_core(C* dst, const C* src, int cl, int cr, int lcr, int tid) {
+  constexpr int MS = LD * LD;
+  const int np = cl * cr;
+  for (int e = tid; e < 2 * np; e += TEAM) {
+    const int sidx = e >= np, r = e - sidx * np;
+    async_elem(dst + sidx * MS + (r >> lcr) * LD + (r & (cr - 1)), src + e);
+  }
+}
+// n contiguous complex elements (element granularity: offsets are only element-aligned)
+template <typename C, int TEAM>
+__device__ __forceinline__ void async_dense(C* dst, const C* src, int n, int tid) {
+  for (int e = tid; e < n; e += TEAM) async_elem(dst + e, src + e);
 }
 __device__ __forceinline__ void blob_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -595,6 +625,9 @@ struct TeamSmem {
     sedge = reinterpret_cast<SEdge<R>*>(b + L_->sedge);
     sbuf = reinterpret_cast<int4*>(b + L_->sbuf);
   }
+  __device__ const int4* sel_sbuf(int buf) const {
+    return reinterpret_cast<const int4*>(base_ + (size_t)buf * L_->dstride + L_->sbuf);
+  }
 };
 
 // BR[t][s'] = sum over staged edges with target t of coef * <s'|O|s> * SRC[src][s]
@@ -922,6 +955,11 @@ lr_sweep(Params p) {
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob);
   int4* const raw0 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw0);
   int4* const raw1 = reinterpret_cast<int4*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.raw1);
+  // direct path: folded cores ping-pong between A / A2 and P lives dense in PIN; both are
+  // cp.async-prefetched one stage ahead (A(q+1) during site q's Lambda GEMM, P(q+1) after
+  // site q's G), so the sweep never waits on HBM/L2 at a site boundary.
+  const bool pf = MODE == 0 && FUSE && p.L.direct;
+  C* const abuf1 = reinterpret_cast<C*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.a2);
   blob_prefetch(raw0, blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
   blob_wait();
   team_sync<TEAM>();
@@ -931,7 +969,15 @@ lr_sweep(Params p) {
     stage_blob<R, TEAM>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
     const int nx = raw0[0].z;
     team_sync<TEAM>();
-    if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
+    if (pf) {
+      async_core<C, LD, TEAM>(sm.A, env_g + s0.a_off, s0.chi_l, s0.chi_r, 31 - __clz(s0.chi_r), tid);
+      async_commit();
+    }
+    if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM, !pf);
+    if (pf) {
+      async_dense<C, TEAM>(PIN, env_g + s0.env_in, s0.rl_db * s0.chi_r * s0.chi_r, tid);
+      async_commit();
+    }
   }
   int cur = 0;
   for (int q = 0; q < seg.site_count; ++q, cur ^= 1) {
@@ -943,17 +989,16 @@ lr_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = MODE == 0 ? st.rl_db : 1;
-    // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM), folded core -> A
-    {
+    C* const Acur = (pf && (q & 1)) ? abuf1 : sm.A;
+    if (pf) {
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // A(q) landed (P(q) may still be in flight)
+    } else {
+      // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM), folded core -> A
       const C* src = env_g + st.env_in;
       const int lper = 2 * lcr;
-      if (!(MODE == 0 && FUSE && p.L.direct)) {
-        for (int e = tid; e < (npin << lper); e += TEAM) {
-          const int ch = e >> lper, r = e & ((1 << lper) - 1);
-          PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
-        }
-      } else if (tid * 32 < (npin << lper)) {
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(src + tid * 32));   // G reads them in-lane later
+      for (int e = tid; e < (npin << lper); e += TEAM) {
+        const int ch = e >> lper, r = e & ((1 << lper) - 1);
+        PIN[ch * MS + (r >> lcr) * LD + (r & (cr - 1))] = src[e];
       }
       const C* ag = env_g + st.a_off;
       const int np = cl * cr;
@@ -967,10 +1012,16 @@ lr_sweep(Params p) {
     STAGE(1);
     if constexpr (FUSE && MODE == 0) {
       // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
-      product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, sm.A, LAM, sm.sedge,
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, Acur, LAM, sm.sedge,
                                               st.lr_edge_count, sm.BR);
       blob_wait();
       team_sync<TEAM>();
+      if (pf && has_next) {   // A(q+1) into the other buffer (A(q) stays live for the Lambda GEMM)
+        const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+        async_core<C, LD, TEAM>((q & 1) ? sm.A : abuf1, env_g + sn.a_off, sn.chi_l, sn.chi_r,
+                                31 - __clz(sn.chi_r), tid);
+        async_commit();
+      }
       STAGE(2);
     } else {
       // M[a][s] = Lam[a] * A[s]
@@ -987,7 +1038,7 @@ lr_sweep(Params p) {
     }
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
     gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2,
-        [&](int, int qq) { return sm.A + qq * MS; },
+        [&](int, int qq) { return Acur + qq * MS; },
         [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
         [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
     int nx2 = -1;
@@ -1014,7 +1065,7 @@ lr_sweep(Params p) {
         if (tid < np) {
           const int al = tid >> lcr, be = tid & (cr - 1);
           C g0 = cmk<C>(R(0), R(0)), g1 = g0;
-          const C* pg = env_g + st.env_in;
+          const C* pg = PIN;   // dense [bb][k][be], prefetched
           for (int bb = 0; bb < db; ++bb) {
             const C* br0 = sm.BR + (bb * 2) * MS + al * LD;
             const C* br1 = br0 + MS;
@@ -1085,7 +1136,13 @@ lr_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(9);
     }
-    if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
+    if (pf && has_next) team_sync<TEAM>();   // every lane is done reading P(q)
+    if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM, !pf);
+    if (pf && has_next) {
+      const tq_site sn = *reinterpret_cast<const tq_site*>(sm.sel_sbuf(cur ^ 1) + 1);
+      async_dense<C, TEAM>(PIN, env_g + sn.env_in, sn.rl_db * sn.chi_r * sn.chi_r, tid);
+      async_commit();
+    }
   }
   STAGE_END(1);
 }
@@ -1391,7 +1448,9 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.m = (int32_t)off; off += (size_t)(fused ? (lr && !L.direct ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
   L.pin = (int32_t)off;
-  if (lr && !L.direct) off += (size_t)D * ms;
+  if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
+  L.a2 = (int32_t)off;
+  if (L.direct) off += 2 * ms;
   L.mr = (int32_t)off;
   if (lr && mode == 1) off += (size_t)2 * D * ms;
   // digit tree (gradient sweep, chi >= 16): per-warp contribution partials; adjoint
