@@ -66,6 +66,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t direct;        // warp teams, one (alpha,beta) pair per lane: G computed in-lane, no G slots;
                          // folded cores (A, A2 ping-pong) and P (dense) are cp.async-prefetched
   int32_t a2;            // second folded-core buffer (direct path)
+  int32_t wc;            // fused path: per-site channel-pair 2x2 bracket matrices + nonzero mask
   int32_t team_bytes;
 };
 
@@ -209,10 +210,10 @@ __device__ __forceinline__ void async_dense(C* dst, const C* src, int n, int tid
 }
 __device__ __forceinline__ void blob_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <typename R, int TEAM>
+template <typename R, int TEAM, int DMW = 0>
 __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_row, const R* coef_row, bool rl, int tid,
                            typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
-                           SEdge<R>* sedge, int4* sbuf) {
+                           SEdge<R>* sedge, int4* sbuf, typename CT<R>::T* wc = nullptr) {
   using C = typename CT<R>::T;
   constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
   constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
@@ -253,6 +254,38 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
     const int4 r = edg[ei];
     SEdge<R> se; se.a = r.x; se.b = r.y; se.op = r.z; se.coef = r.w < 0 ? R(1) : coef_row[r.w];
     sedge[ei] = se;
+  }
+  if constexpr (DMW > 0) {
+    // Channel-pair bracket matrices for the fused stages: W_c[s'][s] = sum coef <s'|O|s> over
+    // the edges of channel pair c = src * DMW + tgt.  Bit c of the trailing mask word says W_c
+    // is nonzero (the stage skips empty pairs).
+    static_assert(TEAM == 32 && 2 * DMW * DMW <= 32, "fused bracket matrices need a warp team");
+    __syncwarp();   // staged edges (coefficients resolved) visible to every lane
+    // lane = (c, s'): each lane folds the edges of its channel pair into one row W_c[s'][.]
+    C wa = cmk<C>(R(0), R(0)), wb = wa;
+    bool any = false;
+    if (tid < 2 * DMW * DMW) {
+      const int cmb = tid >> 1, sp = tid & 1;
+      const int csrc = cmb / DMW, ctgt = cmb % DMW;
+      for (int ei = 0; ei < ec; ++ei) {
+        const SEdge<R> ed = sedge[ei];
+        const int src = rl ? ed.b : ed.a, tgt = rl ? ed.a : ed.b;
+        if (src != csrc || tgt != ctgt) continue;
+        any = true;
+        const int sidx = pauli_src<C>(ed.op, sp);
+        C f = pauli_fac<C>(ed.op, sp);
+        f.x *= ed.coef; f.y *= ed.coef;
+        const R m0 = sidx == 0 ? R(1) : R(0), m1 = R(1) - m0;
+        wa.x = fma(m0, f.x, wa.x); wa.y = fma(m0, f.y, wa.y);
+        wb.x = fma(m1, f.x, wb.x); wb.y = fma(m1, f.y, wb.y);
+      }
+      wc[2 * tid + 0] = wa; wc[2 * tid + 1] = wb;   // = wc[4 * cmb + 2 * sp + {0, 1}]
+    }
+    const unsigned pm = __ballot_sync(0xffffffffu, any);
+    unsigned m = 0;
+#pragma unroll
+    for (int c2 = 0; c2 < DMW * DMW; ++c2) m |= ((pm >> (2 * c2)) & 1u) << c2;
+    if (tid == 0) reinterpret_cast<int*>(wc + 4 * DMW * DMW)[0] = (int)m;
   }
 }
 
@@ -706,9 +739,10 @@ __device__ __forceinline__ C pick(const C (&acc)[DM][2][RT], int idx, int s, int
 template <typename R, int LD, int TEAM, int DM, int RT>
 __device__ void product_bracket(int tid, bool rl, int nsrc, int ntgt, int m, int n, int lm, int ln,
                                 const typename CT<R>::T* A, const typename CT<R>::T* ENV,
-                                const SEdge<R>* sedge, int ec, typename CT<R>::T* BR) {
+                                const typename CT<R>::T* wc, typename CT<R>::T* BR) {
   using C = typename CT<R>::T;
   constexpr int MS = LD * LD;
+  const int wmask = reinterpret_cast<const int*>(wc + 4 * DM * DM)[0];
   const int rt = fused_rows(m, m * n, TEAM, RT);
   const int lrt = rt == 4 ? 2 : (rt == 2 ? 1 : 0);
   const int items = (m >> lrt) << ln;
@@ -764,23 +798,21 @@ __device__ void product_bracket(int tid, bool rl, int nsrc, int ntgt, int m, int
       for (int y = 0; y < 2; ++y)
 #pragma unroll
         for (int z = 0; z < RT; ++z) br[x][y][z] = cmk<C>(R(0), R(0));
-    for (int ei = 0; ei < ec; ++ei) {
-      const SEdge<R> ed = sedge[ei];
-      const int src = rl ? ed.b : ed.a, tgt = rl ? ed.a : ed.b;
+    // BR[t][s'] += W_(src,t)[s'][s] acc[src][s] over the nonzero channel pairs (uniform mask;
+    // every register index is a compile-time constant)
 #pragma unroll
-      for (int sp = 0; sp < 2; ++sp) {
-        const int s = pauli_src<C>(ed.op, sp);
-        C f = pauli_fac<C>(ed.op, sp);
-        f.x *= ed.coef; f.y *= ed.coef;
+    for (int xs = 0; xs < DM; ++xs)
+#pragma unroll
+      for (int xt = 0; xt < DM; ++xt) {
+        if (!((wmask >> (xs * DM + xt)) & 1)) continue;
+        const C* w = wc + 4 * (xs * DM + xt);
+        const C w00 = w[0], w01 = w[1], w10 = w[2], w11 = w[3];
 #pragma unroll
         for (int z = 0; z < RT; ++z) {
-          const C v = cmul(f, pick<C, DM, RT>(acc, src, s, z));
-#pragma unroll
-          for (int x = 0; x < DM; ++x)
-            if (x == tgt) { br[x][sp][z].x += v.x; br[x][sp][z].y += v.y; }
+          cfma(br[xt][0][z], w00, acc[xs][0][z]); cfma(br[xt][0][z], w01, acc[xs][1][z]);
+          cfma(br[xt][1][z], w10, acc[xs][0][z]); cfma(br[xt][1][z], w11, acc[xs][1][z]);
         }
       }
-    }
 #pragma unroll
     for (int x = 0; x < DM; ++x)
       if (x < ntgt)
@@ -802,15 +834,16 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
 // ------------------------------------------------------------------ right-to-left sweep
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
-template <typename R, int CHI, int TEAM, bool FUSED>
+template <typename R, int CHI, int TEAM, int FD>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
-  constexpr bool FUSE = FUSED;                    // register-fused product+bracket (host: chi <= 8 && D <= 4)
-  constexpr int FDM = 4;                          // channels handled by the fused stages
+  constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
+  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
+  constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
@@ -820,6 +853,7 @@ rl_sweep(Params p) {
   if (item >= p.batch * S) return;
   const int b = item / S, g = item % S;
   TeamSmem<R> sm(smem_raw + (size_t)team * p.L.team_bytes, p.L);
+  C* const WC = reinterpret_cast<C*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.wc);
   const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
   const R* coef_b = p.coef ? reinterpret_cast<const R*>(p.coef) + (int64_t)b * p.coef_stride : nullptr;
   C* PIN = sm.ENV;   // P at the right cut (in) / left cut (out)
@@ -843,7 +877,7 @@ rl_sweep(Params p) {
   {
     const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
     sm.sel(0);
-    stage_blob<R, TEAM>(raw0, s0, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
     const int nx = raw0[0].y;
     team_sync<TEAM>();
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
@@ -871,8 +905,7 @@ rl_sweep(Params p) {
     STAGE(1);
     if constexpr (FUSE) {
       // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
-      product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, sm.sedge,
-                                              st.rl_edge_count, sm.BR);
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, WC, sm.BR);
       blob_wait();
       team_sync<TEAM>();
       STAGE(2);
@@ -908,7 +941,7 @@ rl_sweep(Params p) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].y;
       sm.sel(cur ^ 1);
-      stage_blob<R, TEAM>(raw0, sn, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
     }
     team_sync<TEAM>();
     STAGE(4);
@@ -921,7 +954,7 @@ rl_sweep(Params p) {
 // ------------------------------------------------------------------ left-to-right sweep
 // MODE 0: gradient (G + column adjoint); MODE 1: per-term values.  Separate instantiations
 // keep each kernel's code small enough for the instruction cache.
-template <typename R, int CHI, int TEAM, int MODE, bool FUSED>
+template <typename R, int CHI, int TEAM, int MODE, int FD>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
 lr_sweep(Params p) {
   using C = typename CT<R>::T;
@@ -929,8 +962,9 @@ lr_sweep(Params p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
-  constexpr bool FUSE = FUSED;                    // register-fused product+bracket (host: chi <= 8 && D <= 4)
-  constexpr int FDM = 4;                          // channels handled by the fused stages
+  constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
+  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
+  constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = 1;                          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
@@ -940,6 +974,7 @@ lr_sweep(Params p) {
   if (item >= p.batch * S) return;
   const int b = item / S, g = item % S;
   TeamSmem<R> sm(smem_raw + (size_t)team * p.L.team_bytes, p.L);
+  C* const WC = reinterpret_cast<C*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.wc);
   const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
   const R* coef_b = p.coef ? reinterpret_cast<const R*>(p.coef) + (int64_t)b * p.coef_stride : nullptr;
   C* LAM = sm.ENV;
@@ -966,7 +1001,7 @@ lr_sweep(Params p) {
   {
     const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
     sm.sel(0);
-    stage_blob<R, TEAM>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
     const int nx = raw0[0].z;
     team_sync<TEAM>();
     if (pf) {
@@ -1012,8 +1047,7 @@ lr_sweep(Params p) {
     STAGE(1);
     if constexpr (FUSE && MODE == 0) {
       // fused: M[a][s] = Lam[a] A[s] kept in registers, brackets written directly
-      product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, Acur, LAM, sm.sedge,
-                                              st.lr_edge_count, sm.BR);
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, false, da, db, cl, cr, lcl, lcr, Acur, LAM, WC, sm.BR);
       blob_wait();
       team_sync<TEAM>();
       if (pf && has_next) {   // A(q+1) into the other buffer (A(q) stays live for the Lambda GEMM)
@@ -1046,7 +1080,7 @@ lr_sweep(Params p) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].z;
       sm.sel(cur ^ 1);
-      stage_blob<R, TEAM>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
       sm.sel(cur);
     }
     if constexpr (MODE == 0) {
@@ -1451,6 +1485,9 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
   L.a2 = (int32_t)off;
   if (L.direct) off += 2 * ms;
+  off = align_up(off, 16);
+  L.wc = (int32_t)off;
+  if (fused) { const int dm = D <= 3 ? 3 : 4; off += align_up((size_t)dm * dm * 4 * csz + 16, 16); }
   L.mr = (int32_t)off;
   if (lr && mode == 1) off += (size_t)2 * D * ms;
   // digit tree (gradient sweep, chi >= 16): per-warp contribution partials; adjoint
@@ -1540,7 +1577,7 @@ static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rs
   return A;
 }
 
-template <typename R, int CHI, bool FUSED>
+template <typename R, int CHI, int FUSED>
 static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
   constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
@@ -1568,8 +1605,8 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
       cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 0, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       lr_sweep<R, CHI, TEAM, 0, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
     } else {
-      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      lr_sweep<R, CHI, TEAM, 1, false><<<grid, TEAM * TEAMS, smem, s>>>(q);
+      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      lr_sweep<R, CHI, TEAM, 1, 0><<<grid, TEAM * TEAMS, smem, s>>>(q);
     }
     if (g_timing.on) cudaEventRecord(g_timing.ev[3], s);
     cudaError_t e = cudaGetLastError();
@@ -1594,8 +1631,11 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
 // shared-memory layout in make_layout makes the same decision).
 template <typename R, int CHI>
 static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
-  if (CHI <= 8 && prm.c.d_max <= 4) return launch_pair_f<R, CHI, CHI <= 8>(prm, run_lr, s);
-  return launch_pair_f<R, CHI, false>(prm, run_lr, s);
+  if constexpr (CHI <= 8) {
+    if (prm.c.d_max <= 3) return launch_pair_f<R, CHI, 3>(prm, run_lr, s);
+    if (prm.c.d_max <= 4) return launch_pair_f<R, CHI, 4>(prm, run_lr, s);
+  }
+  return launch_pair_f<R, CHI, 0>(prm, run_lr, s);
 }
 
 template <typename R>

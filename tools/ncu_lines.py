@@ -42,14 +42,17 @@ for line in dis.splitlines():
         funcs[cur].append(line)
 demangled = subprocess.run(["c++filt"], input="\n".join(funcs), capture_output=True, text=True).stdout.split("\n")
 want = None
+
+
+def norm(name):
+    return name.replace("(int)", "").replace("(bool)1", "true").replace("(bool)0", "false").replace(" ", "")
+
+
 for mang, dem in zip(funcs, demangled):
-    if re.search(kre, dem) and kname.replace("(int)", "").replace(" ", "") == dem.replace(" ", "").replace("(int)", ""):
+    if re.search(kre, dem) and norm(kname) == norm(dem):
         want = mang
 if want is None:
-    for mang, dem in zip(funcs, demangled):
-        if re.search(kre, dem):
-            want = mang
-            break
+    sys.exit(f"no cubin function matches {kname!r}")
 lines = {}
 curline = None
 for l in funcs[want]:
