@@ -259,8 +259,11 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
     // Channel-pair bracket matrices for the fused stages: W_c[s'][s] = sum coef <s'|O|s> over
     // the edges of channel pair c = src * DMW + tgt.  Bit c of the trailing mask word says W_c
     // is nonzero (the stage skips empty pairs).
-    static_assert(TEAM == 32 && 2 * DMW * DMW <= 32, "fused bracket matrices need a warp team");
-    __syncwarp();   // staged edges (coefficients resolved) visible to every lane
+    static_assert(2 * DMW * DMW <= 32, "fused bracket matrices are built by one warp");
+    // staged edges (coefficients resolved) must be visible to the building warp: when warp 0
+    // staged all of them a warp barrier suffices, otherwise the whole team synchronises
+    if (TEAM == 32 || ec > 32) team_sync<TEAM>();
+    else if (tid < 32) __syncwarp();
     // lane = (c, s'): each lane folds the edges of its channel pair into one row W_c[s'][.]
     C wa = cmk<C>(R(0), R(0)), wb = wa;
     bool any = false;
@@ -281,11 +284,13 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
       }
       wc[2 * tid + 0] = wa; wc[2 * tid + 1] = wb;   // = wc[4 * cmb + 2 * sp + {0, 1}]
     }
-    const unsigned pm = __ballot_sync(0xffffffffu, any);
-    unsigned m = 0;
+    if (tid < 32) {
+      const unsigned pm = __ballot_sync(0xffffffffu, any);
+      unsigned m = 0;
 #pragma unroll
-    for (int c2 = 0; c2 < DMW * DMW; ++c2) m |= ((pm >> (2 * c2)) & 1u) << c2;
-    if (tid == 0) reinterpret_cast<int*>(wc + 4 * DMW * DMW)[0] = (int)m;
+      for (int c2 = 0; c2 < DMW * DMW; ++c2) m |= ((pm >> (2 * c2)) & 1u) << c2;
+      if (tid == 0) reinterpret_cast<int*>(wc + 4 * DMW * DMW)[0] = (int)m;
+    }
   }
 }
 
@@ -844,7 +849,7 @@ rl_sweep(Params p) {
   constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
   constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
   constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
-  constexpr int FRT = 1;                          // rows per fused item
+  constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -965,7 +970,7 @@ lr_sweep(Params p) {
   constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
   constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
   constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
-  constexpr int FRT = 1;                          // rows per fused item
+  constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
@@ -1631,6 +1636,8 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
 // shared-memory layout in make_layout makes the same decision).
 template <typename R, int CHI>
 static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
+  // chi >= 16: the register-fused stages were measured slower than GEMM + bracket
+  // (profiles/r01_stages_cfg4.txt), so they stay unfused
   if constexpr (CHI <= 8) {
     if (prm.c.d_max <= 3) return launch_pair_f<R, CHI, 3>(prm, run_lr, s);
     if (prm.c.d_max <= 4) return launch_pair_f<R, CHI, 4>(prm, run_lr, s);
