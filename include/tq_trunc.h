@@ -1,0 +1,58 @@
+/*
+ * tq_trunc.h — C ABI of the truncated tensor-train engine.
+ *
+ *   tq_tt_simulate  replaces  simulate_tt(circuit, eps, chi_max)        tt.py:237-244
+ *                             (apply_gate_tt tt.py:186-234, _apply_adjacent tt.py:168-183,
+ *                              _split_matrix / _truncate_spectrum tt.py:85-115,
+ *                              _position_center tt.py:146-161)
+ *                   followed by the per-term windows of _expval_tt     hamiltonians.py:129-164
+ *                   for every theta-set of a batch.
+ *
+ * Gates come from the host compiler (paper_2112_10239_b200/truncated.py): one- and two-site
+ * gates on adjacent sites, SWAP chains already expanded, matrix axes in site order.  A
+ * trainable rotation (rot != 0) is evaluated from theta[b][slot] on the device.
+ *
+ * Per theta-set outputs: values [B][T] (re, im float64) = <psi|P_t|psi> (1 for an empty
+ * term, as the reference), discarded [B] (accumulated discarded weight), norm2 [B] (<psi|psi>,
+ * optional), bonds [B][n+1]
+ * (final bond dimensions), flags [B] (1 when a bond needed more than chi_cap).
+ * dtype: TQ_C64 -> theta float32, TQ_C128 -> float64.
+ */
+#ifndef TQ_TRUNC_H
+#define TQ_TRUNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "tq_engine.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One gate of the expanded TEBD program (truncated.py TGATE_DTYPE, 288 bytes). */
+typedef struct {
+  int32_t kind;      /* 1: one-site on `site`; 2: two-site on (site, site + 1) */
+  int32_t site;
+  int32_t rot;       /* 0: constant matrix m; 1 rx, 2 ry, 3 rz, 4 crz from theta[slot] */
+  int32_t slot;
+  int32_t flip;      /* rot == crz with reversed wires: swap the two tensor legs */
+  int32_t pad[3];
+  double m[32];      /* 2x2 or 4x4 complex, row-major, (re, im) interleaved */
+} tq_tgate;
+
+/* Workspace for `batch` theta-sets of an n-qubit train with bond capacity chi_cap (<= 32). */
+size_t tq_tt_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype);
+
+tq_status tq_tt_simulate(int n_qubits, const void* gates, int n_gates, int dtype, int batch,
+                         const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
+                         const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
+                         const int8_t* codes, int n_terms, void* values, double* discarded,
+                         double* norm2, int32_t* bonds, int32_t* flags, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TQ_TRUNC_H */

@@ -22,7 +22,7 @@ __all__ = [
     "tfim_terms", "ry_cz_layers", "brickwork", "tfim_workload_gates",
     "simulate_dense", "expval_dense", "dense_term_values",
     "TT", "tt_zero", "apply_gate_tt", "simulate_tt", "canonicalize",
-    "expval_tt", "tt_inner", "tt_to_dense", "tt_from_product",
+    "expval_tt", "tt_term_values", "tt_inner", "tt_to_dense", "tt_from_product",
     "grad_expval_tt", "taped_term_values", "evaluate_expval",
     "parameter_shift_grad", "finite_diff_grad",
     "mbe_encode", "mbe_objective", "vertex_expectations", "round_cut", "cut_value",

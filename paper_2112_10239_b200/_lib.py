@@ -86,13 +86,19 @@ def load(path: str | None = None):
         lib.tq_abi_layout.argtypes = [ctypes.POINTER(i32), i32]
         lib.tq_build_info.restype = ctypes.c_char_p
         lib.tq_build_info.argtypes = []
+        lib.tq_tt_workspace_bytes.restype = sz
+        lib.tq_tt_workspace_bytes.argtypes = [i32, i32, i32, i32]
+        lib.tq_tt_simulate.restype = i32
+        lib.tq_tt_simulate.argtypes = [i32, vp, i32, i32, i32, vp, i64, ctypes.c_double, i32, i32,
+                                       vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
         _lib = lib
         return lib
 
 
 EXPORTED_SYMBOLS = ("tq_workspace_bytes", "tq_energy_grad", "tq_energy_grad_timed", "tq_ffma_peak",
                     "tq_term_values", "tq_inner",
-                    "tq_status_string", "tq_last_error", "tq_abi_layout", "tq_build_info")
+                    "tq_status_string", "tq_last_error", "tq_abi_layout", "tq_build_info",
+                    "tq_tt_workspace_bytes", "tq_tt_simulate")
 
 
 def check(status: int):

@@ -66,6 +66,39 @@ def _check_chi(plan, chi_max):
                          "the B200 engine is exact (eps=0 semantics)")
 
 
+def _truncating(circuit: Circuit, eps: float, chi_max) -> bool:
+    """True when (eps, chi_max) can change the state: the truncated engine (row f3) runs.
+    eps = 0 with chi_max at or above the exact factored bond truncates nothing."""
+    if eps < 0:
+        raise InputError(f"eps must be >= 0, got {eps}")
+    if eps > 0:
+        return True
+    if chi_max is None:
+        return False
+    if int(chi_max) < 1:
+        raise InputError(f"chi_max must be >= 1, got {chi_max}")
+    return int(chi_max) < C.factored_chi(circuit.n_qubits, C.time_gates(circuit))
+
+
+def _truncated_expval(circuit, ham, arr, eps, chi_max, dtype, device):
+    """Forward value through the truncated TT engine (reference simulate_tt + expval,
+    tt.py:237-244 / hamiltonians.py:167-187), every theta-set of arr [B, P] in one launch."""
+    from . import truncated as TR
+
+    terms = _terms(ham, circuit.n_qubits)
+    res = TR.simulate_terms(circuit, terms, arr, eps, chi_max, dtype=dtype, device=device)
+    e = res.energy([c for c, _ in terms])
+    tol = E.residue_tol(dtype, sum(abs(c) for c, _ in terms))
+    worst = float(np.max(np.abs(e.imag))) if e.size else 0.0
+    if not np.all(np.isfinite(e)):
+        from .errors import NotFinite
+        raise NotFinite("engine produced NaN or Inf")
+    if worst > tol:
+        from .errors import NonHermitianResidue
+        raise NonHermitianResidue(f"imaginary residue {worst:.3e} exceeds {tol:.0e}")
+    return e.real
+
+
 def _device(device):
     if device is None:
         if not torch.cuda.is_available():
@@ -112,6 +145,9 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
     1-D theta -> (float, float64[P]); 2-D theta [B,P] -> (float64[B], float64[B,P])."""
     _check_engine(engine)
     arr, single = _check_theta(circuit, theta)
+    if _truncating(circuit, eps, chi_max):
+        raise InputError("gradients through a truncated split are not supported (the reference's are "
+                         "straight-through, autodiff.py:10-13); use eps=0 and chi_max >= the exact bond")
     dev = _device(device)
     terms = _terms(ham, circuit.n_qubits)
     dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)
@@ -129,9 +165,14 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
 
 def evaluate_expval(circuit: Circuit, ham: PauliHamiltonian, theta=None, engine: str = "tt", eps: float = 0.0,
                     chi_max=None, *, dtype: str = "complex64", device=None, segments=None):
-    """Forward-only <H> (reference autodiff.py:490-503): one right-to-left sweep, nothing stored."""
+    """Forward-only <H> (reference autodiff.py:490-503): one right-to-left sweep, nothing stored.
+    With truncation requested (eps > 0, or chi_max below the exact bond) the truncated TT
+    engine runs instead (row f3, ``truncated.py``)."""
     _check_engine(engine)
     arr, single = _check_theta(circuit, circuit.params() if theta is None else theta)
+    if _truncating(circuit, eps, chi_max):
+        v = _truncated_expval(circuit, ham, arr, eps, chi_max, dtype, device)
+        return float(v[0]) if single else v
     dev = _device(device)
     terms = _terms(ham, circuit.n_qubits)
     dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)
@@ -191,7 +232,8 @@ def parameter_shift_grad(circuit: Circuit, ham: PauliHamiltonian, theta, engine:
     grad = np.zeros(len(th))
     if not rows:
         return grad
-    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), dtype=dtype, device=device))
+    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), eps=eps, chi_max=chi_max, dtype=dtype,
+                                      device=device))
     for k, idx in plan_rows:
         if names[k] == "crz":
             grad[k] = _CRZ_Y1 * (e[idx[0]] - e[idx[1]]) - _CRZ_Y2 * (e[idx[2]] - e[idx[3]])
@@ -215,7 +257,8 @@ def finite_diff_grad(circuit: Circuit, ham: PauliHamiltonian, theta, step: float
         rows += [up, dn]
     if not rows:
         return np.zeros(0)
-    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), dtype=dtype, device=device))
+    e = np.atleast_1d(evaluate_expval(circuit, ham, np.array(rows), eps=eps, chi_max=chi_max, dtype=dtype,
+                                      device=device))
     return (e[0::2] - e[1::2]) / (2 * step)
 
 

@@ -10,13 +10,17 @@ Mirrors ``tnsim.cli`` (``cli.py:70-160,238-248,274-332``):
 Differences:
 - ``--engine`` takes ``b200`` (also ``tt``, an alias).  The reference's ``dense`` engine is
   its CPU oracle.
-- ``--eps`` / ``--chi`` are accepted only where they truncate nothing (the engine is exact).
+- ``--eps`` / ``--chi`` select the truncated TT engine (row f3) whenever they can truncate.
+  ``grad --method ad`` then raises an input error: the reference's gradient through a
+  truncated split is straight-through (autodiff.py:10-13).  ``shift`` and ``fd`` work as in
+  the reference, on truncated forwards.
 - ``ptrace`` and ``paths`` (density matrices, contraction-order search) are outside the hot
   path and are not offered.
 - ``--dtype`` picks complex128 (default, the reference's precision) or complex64.
-- ``simulate`` reports the norm and the factored bond profile.  For n <= 8 it also reports
-  the amplitudes <x|psi>, each computed on the GPU as a batched inner product against
-  the basis product states.
+- ``simulate`` reports the norm, bond dimensions and discarded weight of the truncated
+  engine's run.  That run repeats the reference's simulate_tt.  For n <= 8, when nothing
+  was discarded, it also reports the amplitudes <x|psi>, each computed on the GPU as a
+  batched inner product against the basis product states.
 
 Run as ``python -m paper_2112_10239_b200.cli ...``.
 """
@@ -53,9 +57,7 @@ def _read_json(path: str) -> dict:
 
 
 def _engine_kwargs(args) -> dict:
-    if args.eps != 0.0:
-        raise InputError("the B200 engine is exact; --eps truncation (SURVEY.md row f3) is not available")
-    return {"chi_max": args.chi, "dtype": args.dtype}
+    return {"eps": args.eps, "chi_max": args.chi, "dtype": args.dtype}
 
 
 def _load(args, ham: bool = True):
@@ -99,7 +101,7 @@ def _cmd_grad(args) -> RunReport:
         if args.method == "shift":
             g = AD.parameter_shift_grad(circuit, ham, theta, **kw)
         else:
-            g = AD.finite_diff_grad(circuit, ham, theta, dtype=args.dtype)
+            g = AD.finite_diff_grad(circuit, ham, theta, eps=args.eps, chi_max=args.chi, dtype=args.dtype)
         return evaluate_expval(circuit, ham, theta, **kw), g
 
     (value, grad), ms, peak = measure(run)
@@ -129,21 +131,30 @@ def amplitudes(circuit, dtype: str = "complex128") -> np.ndarray:
 
 def _cmd_simulate(args) -> RunReport:
     from . import autodiff as AD
+    from . import truncated as TR
+    from .errors import BondTooLarge
 
     circuit, _ = _load(args, ham=False)
-    _engine_kwargs(args)
-    bonds = bond_profile(circuit)
-    if args.chi is not None and max(bonds) > args.chi:
-        raise InputError(f"--chi {args.chi} is below the exact bond {max(bonds)} (truncation is row f3)")
-    small = circuit.n_qubits <= AMPLITUDE_DUMP_LIMIT
+    truncating = AD._truncating(circuit, args.eps, args.chi)
 
     def run():
-        nrm2 = AD.state_inner_product(circuit, circuit.params(), circuit, circuit.params(), dtype=args.dtype)
-        return float(np.sqrt(max(float(np.real(nrm2)), 0.0))), (amplitudes(circuit, args.dtype) if small else None)
+        try:   # the truncated engine repeats the reference's simulate_tt: same bonds, weight, norm
+            res = TR.simulate_terms(circuit, [], circuit.params()[None, :], args.eps, args.chi, dtype=args.dtype)
+            bonds, disc, nrm2 = [int(x) for x in res.bonds[0]], float(res.discarded[0]), float(res.norm2[0])
+        except BondTooLarge:
+            if truncating:
+                raise
+            nrm2 = float(np.real(AD.state_inner_product(circuit, circuit.params(), circuit, circuit.params(),
+                                                        dtype=args.dtype)))
+            bonds, disc = bond_profile(circuit), 0.0
+        # amplitudes of the exact state: identical to the truncated one when nothing was discarded
+        small = circuit.n_qubits <= AMPLITUDE_DUMP_LIMIT and (not truncating or disc < 1e-24)
+        amps = amplitudes(circuit, args.dtype) if small else None
+        return float(np.sqrt(max(nrm2, 0.0))), bonds, disc, amps
 
-    (norm, amps), ms, peak = measure(run)
+    (norm, bonds, disc, amps), ms, peak = measure(run)
     outputs = {"n_qubits": circuit.n_qubits, "engine": args.engine, "norm": norm, "bond_dims": bonds,
-               "discarded_weight": 0.0}
+               "discarded_weight": disc}
     if amps is not None:
         outputs["amplitudes"] = [[float(a.real), float(a.imag)] for a in amps]
     return RunReport("simulate", args.seed,
@@ -181,8 +192,8 @@ def _common(sp) -> None:
 
 def _engine(sp) -> None:
     sp.add_argument("--engine", choices=("b200", "tt"), default="b200")
-    sp.add_argument("--chi", type=int, default=None, help="bond cap (must not truncate)")
-    sp.add_argument("--eps", type=float, default=0.0, help="must be 0 (exact engine)")
+    sp.add_argument("--chi", type=int, default=None, help="TT bond cap (truncated engine when it binds)")
+    sp.add_argument("--eps", type=float, default=0.0, help="TT relative truncation threshold")
 
 
 def build_parser() -> argparse.ArgumentParser:

@@ -1459,7 +1459,7 @@ __global__ void ffma_probe(float* out, int iters, float seed) {
 }
 
 // ------------------------------------------------------------------ host side
-static thread_local char g_err[512];
+thread_local char g_err[512];   // shared with tq_trunc.cu
 
 static tq_status fail(tq_status s, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);

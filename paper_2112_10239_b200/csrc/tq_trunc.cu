@@ -1,0 +1,666 @@
+// tq_trunc.cu — truncated tensor-train engine for sm_100a.
+//
+// One CTA per theta-set runs the whole TEBD program of the reference's simulate_tt
+// (tt.py:186-244) on a train held in HBM, then evaluates every Pauli term's window.
+// - One-site gates act in place on their core.  A single-site unitary preserves every
+//   isometry, so the reference's centre move before it (tt.py:205-208) only changes the
+//   gauge and is skipped.
+// - Before a two-site gate the orthogonality centre moves onto the gate's left site
+//   through isometric splits, which replace the reference's QR steps (tt.py:118-161).
+// - The merged two-site block is split by a one-sided (Hestenes) Jacobi SVD in shared
+//   memory.  Sigma goes to the thin side, and the spectrum is cut by the reference rule
+//   (tt.py:85-115): sigma_i / sigma_max > eps, at most chi_max, renormalised by the kept
+//   weight.  Rotations accumulate in V, so the isometric factor is exactly unitary even
+//   when singular values vanish (the reference's eps = 0 keeps exact zeros).
+// - Term values use full left/right norm environments plus one window per term
+//   (hamiltonians.py:129-164).
+// tests/mirror_trunc.py is the numpy mirror of exactly this algorithm.
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/tq_trunc.h"
+
+namespace tq {
+extern thread_local char g_err[512];
+}
+
+namespace tqt {
+
+template <typename R> struct CT;
+template <> struct CT<float> { using T = float2; };
+template <> struct CT<double> { using T = double2; };
+
+template <typename C> __device__ __forceinline__ C cmk(decltype(C::x) x, decltype(C::x) y) { C r; r.x = x; r.y = y; return r; }
+template <typename C> __device__ __forceinline__ C cconj(C a) { return cmk<C>(a.x, -a.y); }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) { return cmk<C>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+template <typename C> __device__ __forceinline__ void cfma(C& acc, C a, C b) {   // acc += a b
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+}
+template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {  // acc += conj(a) b
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
+}
+
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
+
+template <typename R>
+__device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// deterministic block-wide sum (fixed order: lanes, then warps)
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NW; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+struct Params {
+  int n, n_gates, batch, chi_cap, chi_max, n_terms;
+  const tq_tgate* gates;
+  const void* theta;
+  int64_t theta_stride;
+  double eps;
+  const int32_t *term_lo, *term_hi, *code_off;
+  const int8_t* codes;
+  double2* values;
+  double* discarded;
+  double* norm2;
+  int32_t* bonds;
+  int32_t* flags;
+  void* cores;     // [B][n][2 cap^2] complex
+  void* envl;      // [B][n+1][cap^2]
+  void* envr;      // [B][n+1][cap^2]
+};
+
+// Shared scratch of one CTA: X and V are (2cap) x (2cap) complex, column-major with leading
+// dimension 2cap (Jacobi columns are contiguous, rows are spread over lanes).
+template <typename R, int CAP>
+struct Scratch {
+  using C = typename CT<R>::T;
+  static constexpr int LD = 2 * CAP;
+  C X[LD * LD];
+  C V[LD * LD];
+  C G[16];
+  R nrm[LD];
+  int perm[LD];
+  double dred[NT / 32];
+  int k;         // kept rank of the last split
+  R scale;       // renormalisation of the kept weight
+  double disc;   // discarded weight of the last split
+};
+
+// Orthogonalise the ncols columns (length nrows) of X; V (ncols x ncols) accumulates the
+// rotations (X_out = X_in V).  Parallel round-robin ordering: one warp per column pair.
+template <typename R, int CAP>
+__device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const R tol = sizeof(R) == 8 ? R(1e-14) : R(1e-6);
+  const R tiny = sizeof(R) == 8 ? R(1e-280) : R(1e-35);
+  const int max_sweeps = sizeof(R) == 8 ? 40 : 20;
+  for (int e = tid; e < ncols * ncols; e += NT) {
+    const int col = e / ncols, row = e - col * ncols;
+    s.V[col * LD + row] = cmk<C>(row == col ? R(1) : R(0), R(0));
+  }
+  // squared Frobenius norm: a column below eps_mach * ||X|| is numerically zero, and rotating
+  // pairs of such columns never converges in low precision (eps = 0 keeps exact zeros)
+  double fro = 0.0;
+  for (int e = tid; e < ncols * nrows; e += NT) {
+    const int col = e / nrows, row = e - col * nrows;
+    const C u = s.X[col * LD + row];
+    fro += double(u.x) * u.x + double(u.y) * u.y;
+  }
+  fro = block_sum(fro, s.dred);
+  const R floor2 = R(fro * (sizeof(R) == 8 ? 1e-30 : 1e-13));
+  if (ncols < 2) return;
+  const int np = ncols + (ncols & 1);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int any = 0;
+    for (int round = 0; round < np - 1; ++round) {
+      for (int pi = warp; pi < np / 2; pi += NW) {
+        int p, q;
+        if (pi == 0) { p = round; q = np - 1; }
+        else { p = (round + pi) % (np - 1); q = (round - pi + np - 1) % (np - 1); }
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q >= ncols) continue;   // bye for an odd column count
+        C* xp = s.X + p * LD;
+        C* xq = s.X + q * LD;
+        R a = R(0), b = R(0);
+        C g = cmk<C>(R(0), R(0));
+        for (int r = lane; r < nrows; r += 32) {
+          const C u = xp[r], v = xq[r];
+          a = fma(u.x, u.x, fma(u.y, u.y, a));
+          b = fma(v.x, v.x, fma(v.y, v.y, b));
+          cfmac(g, u, v);
+        }
+        a = warp_sum(a); b = warp_sum(b); g.x = warp_sum(g.x); g.y = warp_sum(g.y);
+        const R ag = sqrt(g.x * g.x + g.y * g.y);
+        if (!(ag > tol * sqrt(a) * sqrt(b)) || ag < tiny || (a < floor2 && b < floor2)) continue;   // warp-uniform
+        any = 1;
+        const C e = cmk<C>(g.x / ag, g.y / ag);
+        const R zeta = (b - a) / (R(2) * ag);
+        R t;
+        if (fabs(zeta) > R(1e30)) t = R(0.5) / zeta;
+        else t = (zeta >= R(0) ? R(1) : R(-1)) / (fabs(zeta) + sqrt(R(1) + zeta * zeta));
+        const R c = R(1) / sqrt(R(1) + t * t), sn = c * t;
+        const C se = cmk<C>(sn * e.x, sn * e.y);          // s e
+        const C sec = cmk<C>(sn * e.x, -sn * e.y);        // s conj(e)
+        for (int r = lane; r < nrows; r += 32) {
+          const C u = xp[r], v = xq[r];
+          C nu = cmk<C>(c * u.x, c * u.y), nv = cmk<C>(c * v.x, c * v.y);
+          const C m1 = cmul(sec, v), m2 = cmul(se, u);
+          nu.x -= m1.x; nu.y -= m1.y;
+          nv.x += m2.x; nv.y += m2.y;
+          xp[r] = nu; xq[r] = nv;
+        }
+        C* vp = s.V + p * LD;
+        C* vq = s.V + q * LD;
+        for (int r = lane; r < ncols; r += 32) {
+          const C u = vp[r], v = vq[r];
+          C nu = cmk<C>(c * u.x, c * u.y), nv = cmk<C>(c * v.x, c * v.y);
+          const C m1 = cmul(sec, v), m2 = cmul(se, u);
+          nu.x -= m1.x; nu.y -= m1.y;
+          nv.x += m2.x; nv.y += m2.y;
+          vp[r] = nu; vq[r] = nv;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(any)) break;
+  }
+}
+
+// Column norms of X, descending stable ranking into perm, and the kept rank by the reference
+// rule over the first r = min(m, n) values (truncate = false keeps all r, no rescale).
+template <typename R, int CAP>
+__device__ void rank_and_cut(Scratch<R, CAP>& s, int nrows, int ncols, int r, bool truncate,
+                             double eps, int chi_max, int cap, int32_t* flag) {
+  constexpr int LD = Scratch<R, CAP>::LD;
+  const int tid = threadIdx.x;
+  if (tid < ncols) {
+    R acc = R(0);
+    for (int i = 0; i < nrows; ++i) {
+      const auto u = s.X[tid * LD + i];
+      acc = fma(u.x, u.x, fma(u.y, u.y, acc));
+    }
+    s.nrm[tid] = sqrt(acc);
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    const R mine = s.nrm[tid];
+    int rank = 0;
+    for (int i = 0; i < ncols; ++i) {
+      const R o = s.nrm[i];
+      rank += (o > mine) || (o == mine && i < tid);
+    }
+    s.perm[rank] = tid;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double total = 0.0;
+    for (int i = 0; i < r; ++i) { const double v = s.nrm[s.perm[i]]; total += v * v; }
+    int k = r;
+    if (truncate) {
+      const double s0 = s.nrm[s.perm[0]];
+      if (eps > 0.0 && s0 > 0.0) {
+        int cnt = 0;
+        for (int i = 0; i < r; ++i) cnt += double(s.nrm[s.perm[i]]) > eps * s0;
+        k = cnt > 1 ? cnt : 1;
+      }
+      if (chi_max > 0 && k > chi_max) k = chi_max;
+    }
+    if (k > cap) { *flag = 1; k = cap; }
+    double kept = 0.0;
+    for (int i = 0; i < k; ++i) { const double v = s.nrm[s.perm[i]]; kept += v * v; }
+    double disc = 0.0, scale = 1.0;
+    if (truncate && total > 0.0) {
+      disc = 1.0 - kept / total;
+      if (disc < 0.0) disc = 0.0;
+      scale = kept > 0.0 ? sqrt(total / kept) : 1.0;
+    }
+    if (!truncate) { disc = 0.0; scale = 1.0; }
+    if (k < 1) k = 1;
+    s.k = k; s.scale = R(scale); s.disc = disc;
+  }
+  __syncthreads();
+}
+
+// centre c -> c + 1: core_c (2 chi_l x chi_r) = W S with W isometric; S folds into core_{c+1}
+template <typename R, int CAP>
+__device__ void shift_right(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t* flag) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  constexpr int SLOT = 2 * CAP * CAP;
+  const int tid = threadIdx.x;
+  const int cl = dims[c], cr = dims[c + 1], cr2 = dims[c + 2];
+  C* A = cores + (size_t)c * SLOT;
+  C* B = cores + (size_t)(c + 1) * SLOT;
+  const int m = 2 * cl;                          // X = M^H : cr rows x m columns
+  for (int e = tid; e < m * cr; e += NT) {
+    const int j = e / cr, i = e - j * cr;        // M[j][i] = A flat [j * cr + i]
+    s.X[j * LD + i] = cconj(A[e]);
+  }
+  __syncthreads();
+  jacobi<R, CAP>(s, cr, m);
+  const int r = m < cr ? m : cr;
+  rank_and_cut<R, CAP>(s, cr, m, r, false, 0.0, 0, CAP, flag);
+  const int k = s.k;
+  for (int e = tid; e < m * k; e += NT) {        // core_c[(a,s)][rr] = V[perm[rr]][(a,s)]
+    const int row = e / k, rr = e - row * k;
+    A[e] = s.V[s.perm[rr] * LD + row];
+  }
+  __syncthreads();
+  for (int e = tid; e < k * cr; e += NT) {       // S[rr][i] = conj(X[perm[rr]][i]) -> V scratch
+    const int rr = e / cr, i = e - rr * cr;
+    s.V[e] = cconj(s.X[s.perm[rr] * LD + i]);
+  }
+  __syncthreads();
+  const int nb = 2 * cr2;
+  for (int e = tid; e < cr * nb; e += NT) s.X[e] = B[e];   // stage core_{c+1} (cr x 2 cr2)
+  __syncthreads();
+  for (int e = tid; e < k * nb; e += NT) {
+    const int rr = e / nb, col = e - rr * nb;
+    C acc = cmk<C>(R(0), R(0));
+    for (int i = 0; i < cr; ++i) cfma(acc, s.V[rr * cr + i], s.X[i * nb + col]);
+    B[e] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) dims[c + 1] = k;
+  __syncthreads();
+}
+
+// centre c -> c - 1: core_c (chi_l x 2 chi_r) = L Q with Q row-isometric; L folds into core_{c-1}
+template <typename R, int CAP>
+__device__ void shift_left(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t* flag) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  constexpr int SLOT = 2 * CAP * CAP;
+  const int tid = threadIdx.x;
+  const int cl0 = dims[c - 1], cl = dims[c], cr = dims[c + 1];
+  C* A = cores + (size_t)c * SLOT;
+  C* P = cores + (size_t)(c - 1) * SLOT;
+  const int n = 2 * cr;                          // X = M : cl rows x n columns
+  for (int e = tid; e < cl * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    s.X[j * LD + i] = A[e];
+  }
+  __syncthreads();
+  jacobi<R, CAP>(s, cl, n);
+  const int r = cl < n ? cl : n;
+  rank_and_cut<R, CAP>(s, cl, n, r, false, 0.0, 0, CAP, flag);
+  const int k = s.k;
+  for (int e = tid; e < k * n; e += NT) {        // core_c[rr][col] = conj(V[perm[rr]][col])
+    const int rr = e / n, col = e - rr * n;
+    A[e] = cconj(s.V[s.perm[rr] * LD + col]);
+  }
+  __syncthreads();
+  for (int e = tid; e < cl * k; e += NT) {       // L[i][rr] = X[perm[rr]][i] -> V scratch
+    const int i = e / k, rr = e - i * k;
+    s.V[e] = s.X[s.perm[rr] * LD + i];
+  }
+  __syncthreads();
+  const int mp = 2 * cl0;
+  for (int e = tid; e < mp * cl; e += NT) s.X[e] = P[e];   // stage core_{c-1} (2 cl0 x cl)
+  __syncthreads();
+  for (int e = tid; e < mp * k; e += NT) {
+    const int row = e / k, rr = e - row * k;
+    C acc = cmk<C>(R(0), R(0));
+    for (int i = 0; i < cl; ++i) cfma(acc, s.X[row * cl + i], s.V[i * k + rr]);
+    P[e] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) dims[c] = k;
+  __syncthreads();
+}
+
+template <typename R>
+__device__ void gate_matrix(const tq_tgate& g, const R* theta_b, typename CT<R>::T* G) {
+  using C = typename CT<R>::T;
+  const int d = g.kind == 1 ? 2 : 4;
+  for (int i = 0; i < d * d; ++i) G[i] = cmk<C>(R(g.m[2 * i]), R(g.m[2 * i + 1]));
+  if (g.rot == 0) return;
+  const double t = double(theta_b[g.slot]);
+  double sn, cs;
+  sincos(0.5 * t, &sn, &cs);
+  const R c = R(cs), s = R(sn), z = R(0);
+  if (g.rot == 1) { G[0] = cmk<C>(c, z); G[1] = cmk<C>(z, -s); G[2] = cmk<C>(z, -s); G[3] = cmk<C>(c, z); }
+  else if (g.rot == 2) { G[0] = cmk<C>(c, z); G[1] = cmk<C>(-s, z); G[2] = cmk<C>(s, z); G[3] = cmk<C>(c, z); }
+  else if (g.rot == 3) { G[0] = cmk<C>(c, -s); G[1] = cmk<C>(z, z); G[2] = cmk<C>(z, z); G[3] = cmk<C>(c, s); }
+  else {   // crz, control on the first wire; flip swaps the legs
+    for (int i = 0; i < 16; ++i) G[i] = cmk<C>(z, z);
+    G[0] = cmk<C>(R(1), z); G[5] = cmk<C>(R(1), z);
+    G[10] = cmk<C>(c, -s); G[15] = cmk<C>(c, s);
+    if (g.flip) { G[5] = cmk<C>(c, -s); G[10] = cmk<C>(R(1), z); }
+  }
+}
+
+template <typename R, int CAP>
+__device__ void two_site(Scratch<R, CAP>& s, const Params& p, typename CT<R>::T* cores, int32_t* dims, int i,
+                         double& disc_total, int32_t* flag) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  constexpr int SLOT = 2 * CAP * CAP;
+  const int tid = threadIdx.x;
+  const int cl = dims[i], cm = dims[i + 1], cr = dims[i + 2];
+  C* A = cores + (size_t)i * SLOT;
+  C* B = cores + (size_t)(i + 1) * SLOT;
+  const int m = 2 * cl, n = 2 * cr;
+  const bool left_iso = m <= n;                   // sigma to the right (tt.py:112-115)
+  C* As = s.V;
+  C* Bs = s.V + SLOT;
+  for (int e = tid; e < cl * 2 * cm; e += NT) As[e] = A[e];
+  for (int e = tid; e < cm * 2 * cr; e += NT) Bs[e] = B[e];
+  __syncthreads();
+  for (int e = tid; e < cl * cr; e += NT) {
+    const int a = e / cr, b = e - a * cr;
+    C t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = cmk<C>(R(0), R(0));
+    for (int mid = 0; mid < cm; ++mid) {
+      const C a0 = As[(a * 2 + 0) * cm + mid], a1 = As[(a * 2 + 1) * cm + mid];
+      const C b0 = Bs[(mid * 2 + 0) * cr + b], b1 = Bs[(mid * 2 + 1) * cr + b];
+      cfma(t[0], a0, b0); cfma(t[1], a0, b1); cfma(t[2], a1, b0); cfma(t[3], a1, b1);
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      C acc = cmk<C>(R(0), R(0));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cfma(acc, s.G[o * 4 + q], t[q]);
+      const int row = a * 2 + (o >> 1), col = (o & 1) * cr + b;
+      if (left_iso) s.X[row * LD + col] = cconj(acc);   // X = M^H
+      else s.X[col * LD + row] = acc;                   // X = M
+    }
+  }
+  __syncthreads();
+  const int nrows = left_iso ? n : m, ncols = left_iso ? m : n;
+  jacobi<R, CAP>(s, nrows, ncols);
+  rank_and_cut<R, CAP>(s, nrows, ncols, m < n ? m : n, true, p.eps, p.chi_max, p.chi_cap, flag);
+  const int k = s.k;
+  const R sc = s.scale;
+  if (left_iso) {
+    for (int e = tid; e < m * k; e += NT) {       // core_i[(a,s0)][rr] = V[perm[rr]][(a,s0)]
+      const int row = e / k, rr = e - row * k;
+      A[e] = s.V[s.perm[rr] * LD + row];
+    }
+    for (int e = tid; e < k * n; e += NT) {       // core_{i+1}[rr][col] = conj(X[perm[rr]][col]) * scale
+      const int rr = e / n, col = e - rr * n;
+      const C x = s.X[s.perm[rr] * LD + col];
+      B[e] = cmk<C>(x.x * sc, -x.y * sc);
+    }
+  } else {
+    for (int e = tid; e < m * k; e += NT) {       // core_i[(a,s0)][rr] = X[perm[rr]][(a,s0)] * scale
+      const int row = e / k, rr = e - row * k;
+      const C x = s.X[s.perm[rr] * LD + row];
+      A[e] = cmk<C>(x.x * sc, x.y * sc);
+    }
+    for (int e = tid; e < k * n; e += NT) {       // core_{i+1}[rr][col] = conj(V[perm[rr]][col])
+      const int rr = e / n, col = e - rr * n;
+      B[e] = cconj(s.V[s.perm[rr] * LD + col]);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) dims[i + 1] = k;
+  disc_total += s.disc;
+  __syncthreads();
+}
+
+// ---- environments and term windows ---------------------------------------------------------
+// x' [c][d] = sum_{a,s,s'} conj(A[a][s][c]) P[s][s'] x[a][b] A[b][s'][d]   (P = I for code 0)
+template <typename R, int CAP>
+__device__ void left_step(Scratch<R, CAP>& s, const typename CT<R>::T* A, int ca, int cb, int code,
+                          const typename CT<R>::T* x, typename CT<R>::T* out) {
+  using C = typename CT<R>::T;
+  const int tid = threadIdx.x;
+  C* T = s.X;                                     // T[a][(s', d)] = sum_b x[a][b] A[b][s'][d]
+  const int w = 2 * cb;
+  for (int e = tid; e < ca * w; e += NT) {
+    const int a = e / w, col = e - a * w;
+    C acc = cmk<C>(R(0), R(0));
+    for (int b = 0; b < ca; ++b) cfma(acc, x[a * ca + b], A[b * w + col]);
+    T[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < cb * cb; e += NT) {
+    const int c = e / cb, d = e - c * cb;
+    C acc = cmk<C>(R(0), R(0));
+    for (int a = 0; a < ca; ++a) {
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp) {
+        // (P T)[a][(sp, d)] with one nonzero per Pauli row
+        C u;
+        const C t0 = T[a * w + 0 * cb + d], t1 = T[a * w + 1 * cb + d];
+        if (code == 0) u = sp == 0 ? t0 : t1;
+        else if (code == 1) u = sp == 0 ? t1 : t0;
+        else if (code == 2) u = sp == 0 ? cmk<C>(t1.y, -t1.x) : cmk<C>(-t0.y, t0.x);
+        else u = sp == 0 ? t0 : cmk<C>(-t1.x, -t1.y);
+        cfmac(acc, A[a * w + sp * cb + c], u);
+      }
+    }
+    out[e] = acc;
+  }
+  __syncthreads();
+}
+
+// R_k[a][b] = sum_{s,c,d} conj(A[a][s][c]) R[c][d] A[b][s][d]
+template <typename R, int CAP>
+__device__ void right_step(Scratch<R, CAP>& s, const typename CT<R>::T* A, int ca, int cb,
+                           const typename CT<R>::T* rin, typename CT<R>::T* out) {
+  using C = typename CT<R>::T;
+  const int tid = threadIdx.x;
+  C* T = s.X;                                     // T[(b, s)][c] = sum_d R[c][d] A[b][s][d]
+  for (int e = tid; e < 2 * ca * cb; e += NT) {
+    const int bs = e / cb, c = e - bs * cb;
+    C acc = cmk<C>(R(0), R(0));
+    for (int d = 0; d < cb; ++d) cfma(acc, rin[c * cb + d], A[bs * cb + d]);
+    T[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < ca * ca; e += NT) {
+    const int a = e / ca, b = e - a * ca;
+    C acc = cmk<C>(R(0), R(0));
+    for (int sp = 0; sp < 2; ++sp)
+      for (int c = 0; c < cb; ++c) cfmac(acc, A[(a * 2 + sp) * cb + c], T[(b * 2 + sp) * cb + c]);
+    out[e] = acc;
+  }
+  __syncthreads();
+}
+
+template <typename R, int CAP>
+__global__ void __launch_bounds__(NT, 1) tt_simulate(Params p) {
+  using C = typename CT<R>::T;
+  constexpr int SLOT = 2 * CAP * CAP;
+  constexpr int ESLOT = CAP * CAP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Scratch<R, CAP>& s = *reinterpret_cast<Scratch<R, CAP>*>(smem_raw);
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int n = p.n;
+  C* cores = reinterpret_cast<C*>(p.cores) + (size_t)b * n * SLOT;
+  C* envl = reinterpret_cast<C*>(p.envl) + (size_t)b * (n + 1) * ESLOT;
+  C* envr = reinterpret_cast<C*>(p.envr) + (size_t)b * (n + 1) * ESLOT;
+  int32_t* dims = p.bonds + (size_t)b * (n + 1);
+  int32_t* flag = p.flags + b;
+  const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
+  // |0...0>: bond 1 everywhere
+  for (int k = tid; k < n; k += NT) {
+    cores[(size_t)k * SLOT + 0] = cmk<C>(R(1), R(0));
+    cores[(size_t)k * SLOT + 1] = cmk<C>(R(0), R(0));
+  }
+  for (int k = tid; k <= n; k += NT) dims[k] = 1;
+  __syncthreads();
+  int center = 0;
+  double disc = 0.0;
+  for (int gi = 0; gi < p.n_gates; ++gi) {
+    const tq_tgate& g = p.gates[gi];
+    if (tid == 0) gate_matrix<R>(g, theta_b, s.G);
+    __syncthreads();
+    const int site = g.site;
+    if (g.kind == 1) {
+      const int cl = dims[site], cr = dims[site + 1];
+      C* A = cores + (size_t)site * SLOT;
+      for (int e = tid; e < cl * cr; e += NT) {
+        const int a = e / cr, bb = e - a * cr;
+        const C x0 = A[(a * 2 + 0) * cr + bb], x1 = A[(a * 2 + 1) * cr + bb];
+        C y0 = cmk<C>(R(0), R(0)), y1 = y0;
+        cfma(y0, s.G[0], x0); cfma(y0, s.G[1], x1);
+        cfma(y1, s.G[2], x0); cfma(y1, s.G[3], x1);
+        A[(a * 2 + 0) * cr + bb] = y0; A[(a * 2 + 1) * cr + bb] = y1;
+      }
+      __syncthreads();
+      continue;
+    }
+    while (center < site) { shift_right<R, CAP>(s, cores, dims, center, flag); ++center; }
+    while (center > site) { shift_left<R, CAP>(s, cores, dims, center, flag); --center; }
+    const int m = 2 * dims[site], nn = 2 * dims[site + 2];
+    two_site<R, CAP>(s, p, cores, dims, site, disc, flag);
+    center = m <= nn ? site + 1 : site;
+  }
+  if (tid == 0) p.discarded[b] = disc;
+  // norm environments
+  if (tid == 0) { envl[0] = cmk<C>(R(1), R(0)); envr[(size_t)n * ESLOT] = cmk<C>(R(1), R(0)); }
+  __syncthreads();
+  for (int k = 0; k < n; ++k)
+    left_step<R, CAP>(s, cores + (size_t)k * SLOT, dims[k], dims[k + 1], 0, envl + (size_t)k * ESLOT,
+                      envl + (size_t)(k + 1) * ESLOT);
+  if (tid == 0 && p.norm2) p.norm2[b] = double(envl[(size_t)n * ESLOT].x);   // <psi|psi>
+  for (int k = n - 1; k >= 0; --k)
+    right_step<R, CAP>(s, cores + (size_t)k * SLOT, dims[k], dims[k + 1], envr + (size_t)(k + 1) * ESLOT,
+                       envr + (size_t)k * ESLOT);
+  // term windows: x = L_lo, one left step per site (Pauli or identity), closed with R_{hi+1}
+  C* xa = s.V;
+  C* xb = s.V + ESLOT;
+  for (int t = 0; t < p.n_terms; ++t) {
+    const int lo = p.term_lo[t], hi = p.term_hi[t];
+    if (hi < lo) {
+      if (tid == 0) p.values[(size_t)b * p.n_terms + t] = make_double2(1.0, 0.0);
+      continue;
+    }
+    const int c0 = dims[lo];
+    for (int e = tid; e < c0 * c0; e += NT) xa[e] = envl[(size_t)lo * ESLOT + e];
+    __syncthreads();
+    C* cur = xa;
+    C* nxt = xb;
+    for (int k = lo; k <= hi; ++k) {
+      left_step<R, CAP>(s, cores + (size_t)k * SLOT, dims[k], dims[k + 1], p.codes[p.code_off[t] + (k - lo)], cur, nxt);
+      C* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    const int ce = dims[hi + 1];
+    const C* rr = envr + (size_t)(hi + 1) * ESLOT;
+    double re = 0.0, im = 0.0;
+    for (int e = tid; e < ce * ce; e += NT) {   // sum_ab x[a][b] R[a][b]
+      const C x = cur[e], r = rr[e];
+      re += double(x.x) * r.x - double(x.y) * r.y;
+      im += double(x.x) * r.y + double(x.y) * r.x;
+    }
+    __shared__ double red_re[NT], red_im[NT];
+    red_re[tid] = re; red_im[tid] = im;
+    __syncthreads();
+    for (int h = NT / 2; h > 0; h >>= 1) {
+      if (tid < h) { red_re[tid] += red_re[tid + h]; red_im[tid] += red_im[tid + h]; }
+      __syncthreads();
+    }
+    if (tid == 0) p.values[(size_t)b * p.n_terms + t] = make_double2(red_re[0], red_im[0]);
+    __syncthreads();
+  }
+}
+
+template <typename R, int CAP>
+static tq_status launch(const Params& p, cudaStream_t st) {
+  const size_t smem = sizeof(Scratch<R, CAP>);
+  if (smem > 227 * 1024) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "truncated engine: bond capacity %d needs %zu bytes of shared memory", CAP, smem);
+    return TQ_ERR_UNSUPPORTED;
+  }
+  cudaFuncSetAttribute(tt_simulate<R, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tt_simulate<R, CAP><<<p.batch, NT, smem, st>>>(p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "%s", cudaGetErrorString(e));
+    return TQ_ERR_CUDA;
+  }
+  return TQ_OK;
+}
+
+static int cap_bucket(int chi) { int c = 4; while (c < chi) c <<= 1; return c; }
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct WsParts { size_t cores, envl, envr, total; };
+
+static WsParts ws_parts(int n, int batch, int cap, int dtype) {
+  const size_t csz = dtype == TQ_C128 ? 16 : 8;
+  const int c = cap_bucket(cap);
+  WsParts w{};
+  w.cores = 0;
+  w.envl = align256((size_t)batch * n * 2 * c * c * csz);
+  w.envr = w.envl + align256((size_t)batch * (n + 1) * c * c * csz);
+  w.total = w.envr + align256((size_t)batch * (n + 1) * c * c * csz);
+  return w;
+}
+
+}  // namespace tqt
+
+extern "C" {
+
+size_t tq_tt_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype) {
+  if (n_qubits < 1 || batch < 1 || chi_cap < 1) return 0;
+  return tqt::ws_parts(n_qubits, batch, chi_cap, dtype).total;
+}
+
+tq_status tq_tt_simulate(int n_qubits, const void* gates, int n_gates, int dtype, int batch,
+                         const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
+                         const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
+                         const int8_t* codes, int n_terms, void* values, double* discarded,
+                         double* norm2, int32_t* bonds, int32_t* flags, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  using namespace tqt;
+  if (n_qubits < 1 || batch < 1 || n_gates < 0 || n_terms < 0 || chi_cap < 1 || chi_cap > 32 ||
+      (dtype != TQ_C64 && dtype != TQ_C128)) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "tq_tt_simulate: invalid sizes (n=%d batch=%d cap=%d)", n_qubits, batch, chi_cap);
+    return TQ_ERR_INPUT;
+  }
+  const WsParts w = ws_parts(n_qubits, batch, chi_cap, dtype);
+  if (workspace_bytes < w.total) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "tq_tt_simulate: workspace %zu < %zu bytes", workspace_bytes, w.total);
+    return TQ_ERR_WORKSPACE;
+  }
+  Params p{};
+  p.n = n_qubits; p.n_gates = n_gates; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max;
+  p.n_terms = n_terms; p.gates = reinterpret_cast<const tq_tgate*>(gates); p.theta = theta;
+  p.theta_stride = theta_stride; p.eps = eps; p.term_lo = term_lo; p.term_hi = term_hi;
+  p.code_off = code_off; p.codes = codes; p.values = reinterpret_cast<double2*>(values);
+  p.discarded = discarded; p.norm2 = norm2; p.bonds = bonds; p.flags = flags;
+  unsigned char* base = reinterpret_cast<unsigned char*>(workspace);
+  p.cores = base + w.cores; p.envl = base + w.envl; p.envr = base + w.envr;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
+  const int c = cap_bucket(chi_cap);
+  if (dtype == TQ_C128) {
+    if (c <= 4) return launch<double, 4>(p, st);
+    if (c <= 8) return launch<double, 8>(p, st);
+    if (c <= 16) return launch<double, 16>(p, st);
+    return launch<double, 32>(p, st);
+  }
+  if (c <= 4) return launch<float, 4>(p, st);
+  if (c <= 8) return launch<float, 8>(p, st);
+  if (c <= 16) return launch<float, 16>(p, st);
+  return launch<float, 32>(p, st);
+}
+
+}  // extern "C"

@@ -116,22 +116,21 @@ def bond_profile(circuit: Circuit) -> list:
 def bench_tfim(n_qubits: int = 500, n_gates: int = 5000, chi_max: int | None = 16, grad: bool = True,
                eps: float = 0.0, j: float = 1.0, h: float = 1.0, seed: int = 0, *,
                dtype: str = "complex128") -> RunReport:
-    """TFIM energy (and gradient) of ``tfim_workload`` on the B200 engine
+    """TFIM energy (and gradient) of ``tfim_workload`` on the B200 engines
     (reference bench.py:99-156, same inputs/outputs keys).
 
-    The engine is exact, so the reference's truncation knobs are accepted only where they
-    are no-ops: ``eps`` must be 0, and ``chi_max`` may not be below the exact bond (the
-    reference at eps=0 with chi_max >= the Schmidt rank truncates nothing, so the outputs
-    agree).  A real truncation request raises ``InputError``; it is row f3, not built.
-
-    ``max_bond`` / ``bond_histogram`` describe the engine's factored bonds.  These bound the
-    Schmidt rank from above.  The reference's eps=0 bonds keep representable zeros
-    (tt.py:8-10), so those two keys may differ; every value key matches."""
+    The forward phase runs the truncated TT engine (row f3, ``truncated.py``), which repeats
+    the reference's simulate_tt with (eps, chi_max).  ``expval``, ``max_bond``,
+    ``bond_histogram`` and ``discarded_weight`` therefore follow the reference's semantics.
+    The gradient phase runs the exact engine.  It is offered only when (eps, chi_max)
+    truncate nothing: the reference's gradient through a truncated split is straight-through
+    and documented as best-effort (autodiff.py:10-13), so a truncating ``--grad`` run raises
+    ``InputError``."""
     from . import autodiff as AD
+    from . import chain as C
+    from . import truncated as TR
     from .seeding import generator
 
-    if eps != 0.0:
-        raise InputError("the B200 engine is exact; eps>0 truncation (SURVEY.md row f3) is not available")
     wall = {}
 
     def build():
@@ -139,16 +138,23 @@ def bench_tfim(n_qubits: int = 500, n_gates: int = 5000, chi_max: int | None = 1
         return circuit, tfim(n_qubits, j, h), AD.init_params(circuit.n_params, generator(seed))
 
     (circuit, ham, theta), wall["build"], _ = measure(build)
-    bonds = bond_profile(circuit)
-    if chi_max is not None and max(bonds) > int(chi_max):
-        raise InputError(f"chi_max={chi_max} is below the exact bond {max(bonds)}; truncated evolution "
-                         "(SURVEY.md row f3) is not available on the B200 engine")
-    value, wall["forward"], peak = measure(lambda: AD.evaluate_expval(circuit, ham, theta, dtype=dtype))
+    truncating = AD._truncating(circuit, eps, chi_max)
+    if grad and truncating:
+        raise InputError("a gradient through a truncated split is not supported; rerun with --no-grad "
+                         "(or eps=0 and chi_max >= the exact bond)")
+    terms = C.normalize_terms(ham)
+
+    def forward():
+        return TR.simulate_terms(circuit, terms, theta, eps, chi_max, dtype=dtype)
+
+    res, wall["forward"], peak = measure(forward)
+    value = res.energy([c for c, _ in terms])[0].real
+    bonds = [int(x) for x in res.bonds[0]]
     hist = Counter(bonds)
     outputs = {"gate_count": len(circuit.gates), "n_qubits": n_qubits, "n_params": circuit.n_params,
                "chi_max": chi_max, "expval": float(value), "max_bond": int(max(bonds)),
                "bond_histogram": {str(k): int(v) for k, v in sorted(hist.items())},
-               "discarded_weight": 0.0}
+               "discarded_weight": float(res.discarded[0])}
     if grad:
         (gval, gvec), wall["gradient"], pk = measure(lambda: AD.grad_expval(circuit, ham, theta, dtype=dtype))
         peak = max(peak, pk)

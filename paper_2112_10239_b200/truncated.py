@@ -1,0 +1,182 @@
+"""Truncated tensor-train engine: TEBD-style simulation with SVD
+truncation by (eps, chi_max), discarded weight and per-term expectation values, batched over
+theta-sets on the GPU (``csrc/tq_trunc.cu``, C ABI ``include/tq_trunc.h``).
+
+Semantics follow the reference ``simulate_tt`` / ``apply_gate_tt`` (``tt.py:85-244``):
+- gates are applied in circuit order;
+- a non-adjacent two-qubit gate becomes the reference's SWAP chain (``tt.py:229-233``), and
+  every SWAP is truncated by the same rule;
+- each two-site split keeps ``sigma_i / sigma_max > eps`` up to ``chi_max``, renormalises by
+  the retained weight, and puts sigma on the thin side;
+- the discarded weight accumulates per theta-set.
+
+This engine is forward-only.  The reference's gradient through a truncated split is
+straight-through and documented as best-effort (``autodiff.py:10-13``), so gradients stay
+on the exact engine.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from .circuits import Circuit, gate_matrix
+from .errors import BondTooLarge, InputError, UnsupportedArity, WireOutOfRange
+
+TGATE_DTYPE = np.dtype([("kind", "<i4"), ("site", "<i4"), ("rot", "<i4"), ("slot", "<i4"),
+                        ("flip", "<i4"), ("pad", "<i4", (3,)), ("m", "<f8", (32,))])   # 288 bytes
+ROT_CODE = {"rx": 1, "ry": 2, "rz": 3, "crz": 4}
+MAX_CHI_TRUNC = 32          # bond capacity of the kernel (shared-memory split of 2chi x 2chi)
+_SWAP = gate_matrix("swap")
+
+
+def _flip4(m: np.ndarray) -> np.ndarray:
+    return m.reshape(2, 2, 2, 2).transpose(1, 0, 3, 2).reshape(4, 4)
+
+
+def compile_gates(circuit: Circuit):
+    """Circuit -> (gate table [G] TGATE_DTYPE, python list [(matrix-or-None, sites, rot, slot, flip)]).
+
+    Trainable rotations keep their theta slot (the kernel evaluates the matrix per theta-set);
+    everything else is stored as a constant matrix with axes in site order."""
+    n = circuit.n_qubits
+    slot_of = {g: s for s, g in enumerate(circuit.trainable)}
+    rows = []
+    for gi, g in enumerate(circuit.gates):
+        w = tuple(int(x) for x in g.wires)
+        if any(not 0 <= x < n for x in w):
+            raise WireOutOfRange(f"gate '{g.name}' wires {w} exceed n={n}")
+        slot = slot_of.get(gi, -1)
+        rot = ROT_CODE.get(g.name, 0) if slot >= 0 else 0
+        mat = np.asarray(g.matrix, dtype=complex)
+        if len(w) == 1:
+            rows.append((None if rot else mat, (w[0],), rot, slot, 0))
+            continue
+        if len(w) != 2:
+            raise UnsupportedArity(f"TT engine handles 1- and 2-qubit gates, got {len(w)} wires")
+        lo, hi = min(w), max(w)
+        flip = 1 if w[0] > w[1] else 0
+        m4 = None if rot else (_flip4(mat) if flip else mat)
+        for j in range(hi - 1, lo, -1):      # bring hi next to lo (reference tt.py:229-231)
+            rows.append((_SWAP, (j, j + 1), 0, -1, 0))
+        rows.append((m4, (lo, lo + 1), rot, slot, flip if rot else 0))   # constants are pre-flipped
+        for j in range(lo + 1, hi):          # and back
+            rows.append((_SWAP, (j, j + 1), 0, -1, 0))
+    table = np.zeros(len(rows), dtype=TGATE_DTYPE)
+    for r, (m, sites, rot, slot, flip) in enumerate(rows):
+        table[r]["kind"] = len(sites)
+        table[r]["site"] = sites[0]
+        table[r]["rot"] = rot
+        table[r]["slot"] = slot
+        table[r]["flip"] = flip
+        if m is not None:
+            flat = np.asarray(m, dtype=complex).reshape(-1)
+            table[r]["m"][: 2 * flat.size: 2] = flat.real
+            table[r]["m"][1: 2 * flat.size: 2] = flat.imag
+    return table, rows
+
+
+def resolved_gates(rows, theta: np.ndarray):
+    """[(matrix, sites)] for one theta-set (the mirror's input; the kernel does this on device)."""
+    out = []
+    for m, sites, rot, slot, flip in rows:
+        if m is None:
+            name = {1: "rx", 2: "ry", 3: "rz", 4: "crz"}[rot]
+            m = gate_matrix(name, float(theta[slot]))
+            if flip:
+                m = _flip4(m)
+        out.append((m, sites))
+    return out
+
+
+def term_table(terms, n: int):
+    """Normalised terms -> (lo [T], hi [T], code offsets [T+1], codes [sum window] int8)."""
+    code = {"X": 1, "Y": 2, "Z": 3, 1: 1, 2: 2, 3: 3}
+    lo = np.zeros(len(terms), np.int32)
+    hi = np.full(len(terms), -1, np.int32)
+    offs = np.zeros(len(terms) + 1, np.int32)
+    codes = []
+    for t, (_, ops) in enumerate(terms):
+        ops = dict(ops)
+        if ops:
+            lo[t], hi[t] = min(ops), max(ops)
+            codes += [code[ops[k]] if k in ops else 0 for k in range(lo[t], hi[t] + 1)]
+        offs[t + 1] = len(codes)
+    return lo, hi, offs, np.array(codes if codes else [0], np.int8)
+
+
+def check_truncation_args(eps: float, chi_max) -> int:
+    if eps < 0:
+        raise InputError(f"eps must be >= 0, got {eps}")
+    if chi_max is not None and int(chi_max) < 1:
+        raise InputError(f"chi_max must be >= 1, got {chi_max}")
+    # a larger chi_max is accepted; a bond that actually outgrows the capacity raises BondTooLarge
+    return MAX_CHI_TRUNC if chi_max is None else min(int(chi_max), MAX_CHI_TRUNC)
+
+
+class TruncatedResult:
+    """Per-theta-set results of one truncated simulation."""
+
+    def __init__(self, values, discarded, bonds, norm2):
+        self.values = values          # complex128 [B, T]
+        self.discarded = discarded    # float64 [B]
+        self.bonds = bonds            # int32 [B, n+1] final bond dimensions
+        self.norm2 = norm2            # float64 [B] <psi|psi>
+
+    def energy(self, coeffs) -> np.ndarray:
+        """sum_t coeff_t v_t in term order (reference hamiltonians.py:161-164)."""
+        out = np.zeros(self.values.shape[0], dtype=complex)
+        for t, c in enumerate(coeffs):
+            out = out + c * self.values[:, t]
+        return out
+
+
+def simulate_terms(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=None, *,
+                   dtype: str = "complex128", device=None) -> TruncatedResult:
+    """Truncated evolution of every theta-set [B, P] and <P_t> for each normalised term."""
+    import torch
+
+    from . import _lib
+    from .engine import _stream
+
+    cap = check_truncation_args(eps, chi_max)
+    theta = np.atleast_2d(np.asarray(theta, dtype=float))
+    if theta.shape[1] != circuit.n_params:
+        from .errors import ParamCountMismatch
+        raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
+    B, n = theta.shape[0], circuit.n_qubits
+    table, _ = compile_gates(circuit)
+    lo, hi, offs, codes = term_table(terms, n)
+    from .autodiff import _device
+
+    dev = _device(device)   # EngineUnavailable without a GPU: there is no CPU fallback
+    code = _lib.TQ_C128 if dtype == "complex128" else _lib.TQ_C64
+    tdt = torch.float64 if dtype == "complex128" else torch.float32
+    lib = _lib.load()
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    d_gates = up(table.view(np.uint8))
+    d_lo, d_hi, d_offs, d_codes = up(lo), up(hi), up(offs), up(codes)
+    th = torch.tensor(theta, dtype=tdt, device=dev)
+    T = len(terms)
+    values = torch.zeros(B, max(T, 1), 2, dtype=torch.float64, device=dev)
+    disc = torch.zeros(B, dtype=torch.float64, device=dev)
+    norm2 = torch.zeros(B, dtype=torch.float64, device=dev)
+    bonds = torch.zeros(B, n + 1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(B, dtype=torch.int32, device=dev)
+    ws_bytes = lib.tq_tt_workspace_bytes(n, B, cap, code)
+    ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=dev)
+    st = lib.tq_tt_simulate(n, d_gates.data_ptr(), len(table), code, B, th.data_ptr(), th.stride(0),
+                            ctypes.c_double(eps), cap, -1 if chi_max is None else int(chi_max),
+                            d_lo.data_ptr(), d_hi.data_ptr(), d_offs.data_ptr(), d_codes.data_ptr(), T,
+                            values.data_ptr(), disc.data_ptr(), norm2.data_ptr(), bonds.data_ptr(), flags.data_ptr(),
+                            ws.data_ptr(), ctypes.c_size_t(int(ws_bytes)), _stream())
+    _lib.check(st)
+    f = flags.cpu().numpy()
+    if np.any(f):
+        raise BondTooLarge(f"a bond exceeded the truncated engine's capacity chi={cap}; pass chi_max <= {cap}")
+    vals = torch.view_as_complex(values).cpu().numpy()[:, :T]
+    return TruncatedResult(vals, disc.cpu().numpy(), bonds.cpu().numpy(), norm2.cpu().numpy())

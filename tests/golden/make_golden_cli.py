@@ -83,6 +83,18 @@ def main():
         cases.append(("bench", ["bench", "tfim", "--n", "4", "--gates", "25", "--chi", "8", "--seed", "2"], ()))
         cases.append(("bench", ["bench", "tfim", "--n", "6", "--gates", "60", "--chi", "16", "--seed", "4"], ()))
         cases.append(("bench", ["bench", "tfim", "--n", "2", "--gates", "0", "--seed", "0", "--no-grad"], ()))
+        # truncating runs (row f3): chi below the exact bond, eps > 0
+        cases.append(("bench", ["bench", "tfim", "--n", "12", "--gates", "260", "--chi", "4", "--seed", "3",
+                                "--no-grad"], ()))
+        cases.append(("bench", ["bench", "tfim", "--n", "10", "--gates", "300", "--chi", "16", "--eps", "1e-3",
+                                "--seed", "5", "--no-grad"], ()))
+        cases.append(("expval", ["expval", "--circuit", p("mixed"), "--ham", p("h5"), "--engine", "tt",
+                                 "--chi", "2"], ("mixed", "h5", "chi2")))
+        cases.append(("grad", ["grad", "--circuit", p("mixed"), "--ham", p("h5"), "--method", "shift",
+                               "--engine", "tt", "--chi", "2"], ("mixed", "h5", "shift", "chi2")))
+        cases.append(("simulate", ["simulate", "--circuit", p("mixed"), "--engine", "tt", "--chi", "2"],
+                      ("mixed", "chi2")))
+        cases.append(("simulate", ["simulate", "--circuit", p("mixed"), "--engine", "tt"], ("mixed", "tt")))
         for kind, argv, key in cases:
             rep = run(argv)
             runs.append({"kind": kind, "key": list(key), "argv_tail": [a for a in argv if not a.startswith(tmp)],

@@ -75,6 +75,25 @@ def test_grad_methods_match_reference_cli(files, capsys, golden_cli):
     assert abs(rep["outputs"]["gradient"][0] + np.sin(0.7)) < 1e-12   # reference test_cli.py:106-118
 
 
+def test_truncating_runs_match_reference_cli(files, capsys, golden_cli):
+    c, h = str(files / "mixed.json"), str(files / "h5.json")
+    rep = _report(["expval", "--circuit", c, "--ham", h, "--chi", "2"], capsys)
+    assert abs(rep["outputs"]["value"] - _ref(golden_cli, "expval", ("mixed", "h5", "chi2"))["value"]) < 1e-12
+    rep = _report(["grad", "--circuit", c, "--ham", h, "--chi", "2", "--method", "shift"], capsys)
+    ref = _ref(golden_cli, "grad", ("mixed", "h5", "shift", "chi2"))
+    np.testing.assert_allclose(rep["outputs"]["gradient"], ref["gradient"], atol=1e-11)
+    code = cli.run_cli(["grad", "--circuit", c, "--ham", h, "--chi", "2"])   # ad through truncation
+    capsys.readouterr()
+    assert code == 2
+    for key, extra in ((("mixed", "chi2"), ["--chi", "2"]), (("mixed", "tt"), [])):
+        rep = _report(["simulate", "--circuit", c] + extra, capsys)
+        ref = _ref(golden_cli, "simulate", key)
+        assert rep["outputs"]["bond_dims"] == ref["bond_dims"], key
+        assert abs(rep["outputs"]["norm"] - ref["norm"]) < 1e-12
+        assert abs(rep["outputs"]["discarded_weight"] - ref["discarded_weight"]) < 1e-14
+        np.testing.assert_allclose(rep["outputs"]["amplitudes"], ref["amplitudes"], atol=1e-12)
+
+
 def test_simulate_amplitudes_match_reference_dense(files, capsys, golden_cli):
     for c in ("bell", "mixed"):
         rep = _report(["simulate", "--circuit", str(files / f"{c}.json")], capsys)
@@ -89,11 +108,12 @@ def test_bench_tfim_matches_reference(capsys, golden_cli):
     for r in refs:
         i, ref = r["report"]["inputs"], r["report"]["outputs"]
         argv = ["bench", "tfim", "--n", str(i["n"]), "--gates", str(i["gates"]), "--seed", str(r["report"]["seed"])]
-        argv += ["--chi", str(i["chi_max"])] + ([] if i["grad"] else ["--no-grad"])
+        argv += ["--chi", str(i["chi_max"]), "--eps", str(i["eps"])] + ([] if i["grad"] else ["--no-grad"])
         rep = _report(argv, capsys)
         out = rep["outputs"]
-        for k in ("gate_count", "n_qubits", "n_params", "chi_max", "discarded_weight"):
+        for k in ("gate_count", "n_qubits", "n_params", "chi_max", "max_bond", "bond_histogram"):
             assert out[k] == ref[k], k
+        assert abs(out["discarded_weight"] - ref["discarded_weight"]) < 1e-12
         assert abs(out["expval"] - ref["expval"]) < 1e-10
         if i["grad"]:
             assert abs(out["grad_value"] - ref["grad_value"]) < 1e-10
@@ -104,7 +124,7 @@ def test_bench_tfim_matches_reference(capsys, golden_cli):
         rep.pop("measured"), again.pop("measured")
         assert rep == again
     with pytest.raises(InputError):
-        bench_tfim(n_qubits=40, n_gates=2000, chi_max=4, grad=False)   # would truncate: row f3
+        bench_tfim(n_qubits=40, n_gates=2000, chi_max=4, grad=True)    # gradient through truncation
 
 
 def test_maxcut_subcommand(files, capsys):

@@ -1,0 +1,87 @@
+"""Row f3 on the GPU: the truncated TT engine (csrc/tq_trunc.cu) against the reference's own
+truncated simulation (tests/golden/golden_trunc.json from make_golden_trunc.py) and the
+oracle restatement (oracle.simulate_tt), including the numpy mirror of the kernel."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+from helpers_engine import to_circuit, to_ham  # noqa: E402
+from paper_2112_10239_b200 import chain as C  # noqa: E402
+from paper_2112_10239_b200 import truncated as TR  # noqa: E402
+from paper_2112_10239_b200.errors import BondTooLarge  # noqa: E402
+from paper_2112_10239_b200.hamiltonians import tfim  # noqa: E402
+from paper_2112_10239_b200.workloads import layered_circuit, theta_sets  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def golden_trunc():
+    with open(os.path.join(HERE, "golden", "golden_trunc.json")) as f:
+        return json.load(f)
+
+
+def _ocirc(c):
+    return O.OCircuit(c.n_qubits, [(g.name, tuple(g.wires), g.param) for g in c.gates], list(c.trainable))
+
+
+def test_reference_golden_truncated(golden_trunc):
+    for case in golden_trunc["cases"]:
+        c = to_circuit(case["circuit"])
+        h = to_ham(case["ham"], c.n_qubits)
+        terms = C.normalize_terms(h)
+        res = TR.simulate_terms(c, terms, np.array([case["theta"]]), case["eps"], case["chi_max"])
+        e = res.energy([t[0] for t in terms])[0]
+        assert abs(e.real - case["value"]) < 1e-10 * max(1.0, abs(case["value"])), case["name"]
+        assert abs(res.discarded[0] - case["discarded"]) < 1e-10, case["name"]
+        assert res.bonds[0].max() <= (case["chi_max"] or 32)
+        if case.get("bonds_match", True):
+            assert list(res.bonds[0]) == case["bonds"], case["name"]
+
+
+def test_batched_against_oracle_c128_and_c64():
+    c = layered_circuit(12, 12, "ry", "cnot")
+    terms = C.normalize_terms(tfim(12))
+    oterms = O.tfim_terms(12)
+    th = theta_sets(c.n_params, 5, seed=7)
+    for eps, chi in ((0.0, 4), (1e-3, None), (1e-2, 6)):
+        r128 = TR.simulate_terms(c, terms, th, eps, chi, dtype="complex128")
+        r64 = TR.simulate_terms(c, terms, th, eps, chi, dtype="complex64")
+        for b in range(th.shape[0]):
+            tt = O.simulate_tt(_ocirc(c), th[b], eps=eps, chi_max=chi)
+            ov = O.tt_term_values(tt, oterms)
+            np.testing.assert_allclose(r128.values[b], ov, atol=1e-10)
+            assert abs(r128.discarded[b] - tt.discarded) < 1e-10
+            assert list(r128.bonds[b]) == list(tt.bonds)
+            np.testing.assert_allclose(r64.values[b], ov, atol=2e-4)
+
+
+def test_exact_limit_matches_exact_engine():
+    from paper_2112_10239_b200 import autodiff as AD
+
+    c = layered_circuit(16, 8, "ry", "cz")
+    h = tfim(16)
+    terms = C.normalize_terms(h)
+    th = theta_sets(c.n_params, 3, seed=2)
+    res = TR.simulate_terms(c, terms, th, 0.0, None)
+    e = res.energy([t[0] for t in terms]).real
+    ref = AD.evaluate_expval(c, h, th, dtype="complex128")
+    np.testing.assert_allclose(e, ref, atol=1e-10)
+    assert np.all(res.discarded < 1e-20)
+
+
+def test_capacity_overflow_raises():
+    c = layered_circuit(14, 14, "ry", "cnot")
+    terms = C.normalize_terms(tfim(14))
+    with pytest.raises(BondTooLarge):
+        TR.simulate_terms(c, terms, theta_sets(c.n_params, 1, seed=0), 0.0, None)

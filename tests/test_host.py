@@ -97,8 +97,10 @@ def test_library_exports_every_header_symbol():
     import torch  # noqa: F401  (provides libcudart.so.12 to the loader)
     from paper_2112_10239_b200 import _lib
 
-    header = open(os.path.join(ROOT, "include", "tq_engine.h")).read()
-    declared = set(re.findall(r"\b(tq_[a-z_]+)\s*\(", header))
+    declared = set()
+    for h in ("tq_engine.h", "tq_trunc.h"):
+        header = open(os.path.join(ROOT, "include", h)).read()
+        declared |= set(re.findall(r"\b(tq_[a-z_]+)\s*\(", header))
     assert declared == set(_lib.EXPORTED_SYMBOLS)
     lib = ctypes.CDLL(path)
     for sym in declared:

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build the engine and its stage-timing variant in parallel (ptxas -v log in build_ptxas.log).
 cd "$(dirname "$0")/.."
-SRC=paper_2112_10239_b200/csrc/tq_engine.cu
+SRC="paper_2112_10239_b200/csrc/tq_engine.cu paper_2112_10239_b200/csrc/tq_trunc.cu"
 FLAGS="-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -shared -cudart shared -Iinclude -diag-suppress 177,550"
 nvcc $FLAGS -Xptxas -v -o paper_2112_10239_b200/libtq_engine.so.tmp $SRC > build_ptxas.log 2>&1 &
 P1=$!
