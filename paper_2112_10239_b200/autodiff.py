@@ -164,15 +164,17 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
 
 
 def evaluate_expval(circuit: Circuit, ham: PauliHamiltonian, theta=None, engine: str = "tt", eps: float = 0.0,
-                    chi_max=None, *, dtype: str = "complex64", device=None, segments=None):
+                    chi_max=None, *, dtype: str | None = None, device=None, segments=None):
     """Forward-only <H> (reference autodiff.py:490-503): one right-to-left sweep, nothing stored.
     With truncation requested (eps > 0, or chi_max below the exact bond) the truncated TT
     engine runs instead (row f3, ``truncated.py``)."""
     _check_engine(engine)
     arr, single = _check_theta(circuit, circuit.params() if theta is None else theta)
     if _truncating(circuit, eps, chi_max):
-        v = _truncated_expval(circuit, ham, arr, eps, chi_max, dtype, device)
+        # long truncated evolutions accumulate rounding with depth: complex128 unless asked
+        v = _truncated_expval(circuit, ham, arr, eps, chi_max, dtype or "complex128", device)
         return float(v[0]) if single else v
+    dtype = dtype or "complex64"
     dev = _device(device)
     terms = _terms(ham, circuit.n_qubits)
     dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)

@@ -98,6 +98,8 @@ struct Scratch {
   C G[16];
   R nrm[LD];
   int perm[LD];
+  C hdiag[LD];   // Householder QR: diagonal of R
+  R htau[LD];    //                 reflector scales
   double dred[NT / 32];
   int k;         // kept rank of the last split
   R scale;       // renormalisation of the kept weight
@@ -199,7 +201,9 @@ __device__ void rank_and_cut(Scratch<R, CAP>& s, int nrows, int ncols, int r, bo
       const auto u = s.X[tid * LD + i];
       acc = fma(u.x, u.x, fma(u.y, u.y, acc));
     }
-    s.nrm[tid] = sqrt(acc);
+    const R v = sqrt(acc);
+    if (!(v == v)) *flag = 2;                    // NaN: reported as NotFinite by the host
+    s.nrm[tid] = v == v ? v : R(0);              // keep the ranking a permutation
   }
   __syncthreads();
   if (tid < ncols) {
@@ -241,9 +245,87 @@ __device__ void rank_and_cut(Scratch<R, CAP>& s, int nrows, int ncols, int r, bo
   __syncthreads();
 }
 
-// centre c -> c + 1: core_c (2 chi_l x chi_r) = W S with W isometric; S folds into core_{c+1}
+// Householder QR of X (rows x cols, column-major): reflectors overwrite X below the diagonal,
+// R's strict upper triangle stays in X and its diagonal goes to hdiag; Q (rows x k,
+// k = min(rows, cols)) is accumulated into V.  Robust for rank-deficient X (a zero column
+// gets tau = 0, so Q stays exactly isometric), which the reference's eps = 0 zeros need.
 template <typename R, int CAP>
-__device__ void shift_right(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t* flag) {
+__device__ int house_qr(Scratch<R, CAP>& s, int rows, int cols) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = rows < cols ? rows : cols;
+  for (int j = 0; j < k; ++j) {
+    if (warp == 0) {
+      C* x = s.X + j * LD;
+      R sig2 = R(0);
+      for (int r = j + 1 + lane; r < rows; r += 32) sig2 = fma(x[r].x, x[r].x, fma(x[r].y, x[r].y, sig2));
+      sig2 = warp_sum(sig2);
+      const C x0 = x[j];
+      const R a0 = sqrt(x0.x * x0.x + x0.y * x0.y);
+      const R sig = sqrt(sig2 + a0 * a0);
+      if (!(sig >= (sizeof(R) == 8 ? R(1e-150) : R(1e-18)))) {   // numerically zero column (or NaN): H = I
+        if (lane == 0) { s.htau[j] = R(0); s.hdiag[j] = cmk<C>(R(0), R(0)); }
+      } else {
+        const C ph = a0 > R(0) ? cmk<C>(x0.x / a0, x0.y / a0) : cmk<C>(R(1), R(0));
+        const C alpha = cmk<C>(-ph.x * sig, -ph.y * sig);          // H x = alpha e_j
+        const C v0 = cmk<C>(x0.x - alpha.x, x0.y - alpha.y);
+        const R vn2 = sig2 + v0.x * v0.x + v0.y * v0.y;
+        if (lane == 0) { s.htau[j] = R(2) / vn2; s.hdiag[j] = alpha; x[j] = v0; }
+      }
+    }
+    __syncthreads();
+    const R tau = s.htau[j];
+    if (tau != R(0)) {
+      const C* v = s.X + j * LD;
+      for (int c = j + 1 + warp; c < cols; c += NW) {          // X[j:, c] -= tau v (v^H X[j:, c])
+        C* xc = s.X + c * LD;
+        C w = cmk<C>(R(0), R(0));
+        for (int r = j + lane; r < rows; r += 32) cfmac(w, v[r], xc[r]);
+        w.x = warp_sum(w.x); w.y = warp_sum(w.y);
+        w.x *= tau; w.y *= tau;
+        for (int r = j + lane; r < rows; r += 32) { const C t = cmul(v[r], w); xc[r].x -= t.x; xc[r].y -= t.y; }
+      }
+    }
+    __syncthreads();
+  }
+  // Q = H_0 ... H_{k-1} [I_k; 0], backward accumulation, one warp per column
+  for (int e = tid; e < rows * k; e += NT) {
+    const int c = e / rows, r = e - c * rows;
+    s.V[c * LD + r] = cmk<C>(r == c ? R(1) : R(0), R(0));
+  }
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {
+    const R tau = s.htau[j];
+    if (tau != R(0)) {
+      const C* v = s.X + j * LD;
+      for (int c = j + warp; c < k; c += NW) {                  // columns < j are untouched
+        C* qc = s.V + c * LD;
+        C w = cmk<C>(R(0), R(0));
+        for (int r = j + lane; r < rows; r += 32) cfmac(w, v[r], qc[r]);
+        w.x = warp_sum(w.x); w.y = warp_sum(w.y);
+        w.x *= tau; w.y *= tau;
+        for (int r = j + lane; r < rows; r += 32) { const C t = cmul(v[r], w); qc[r].x -= t.x; qc[r].y -= t.y; }
+      }
+    }
+    __syncthreads();
+  }
+  return k;
+}
+
+// element (r, c) of R after house_qr
+template <typename R, int CAP>
+__device__ __forceinline__ typename CT<R>::T house_r(const Scratch<R, CAP>& s, int r, int c) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  if (r == c) return s.hdiag[r];
+  return r < c ? s.X[c * LD + r] : cmk<C>(R(0), R(0));
+}
+
+// centre c -> c + 1 (reference _shift_center_right, tt.py:118-122): core_c (2 chi_l x chi_r)
+// = Q R, Q stays, R folds into core_{c+1}
+template <typename R, int CAP>
+__device__ void shift_right(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t*) {
   using C = typename CT<R>::T;
   constexpr int LD = Scratch<R, CAP>::LD;
   constexpr int SLOT = 2 * CAP * CAP;
@@ -251,33 +333,31 @@ __device__ void shift_right(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_
   const int cl = dims[c], cr = dims[c + 1], cr2 = dims[c + 2];
   C* A = cores + (size_t)c * SLOT;
   C* B = cores + (size_t)(c + 1) * SLOT;
-  const int m = 2 * cl;                          // X = M^H : cr rows x m columns
+  const int m = 2 * cl;
   for (int e = tid; e < m * cr; e += NT) {
-    const int j = e / cr, i = e - j * cr;        // M[j][i] = A flat [j * cr + i]
-    s.X[j * LD + i] = cconj(A[e]);
+    const int row = e / cr, col = e - row * cr;
+    s.X[col * LD + row] = A[e];
   }
   __syncthreads();
-  jacobi<R, CAP>(s, cr, m);
-  const int r = m < cr ? m : cr;
-  rank_and_cut<R, CAP>(s, cr, m, r, false, 0.0, 0, CAP, flag);
-  const int k = s.k;
-  for (int e = tid; e < m * k; e += NT) {        // core_c[(a,s)][rr] = V[perm[rr]][(a,s)]
+  const int k = house_qr<R, CAP>(s, m, cr);
+  for (int e = tid; e < m * k; e += NT) {
     const int row = e / k, rr = e - row * k;
-    A[e] = s.V[s.perm[rr] * LD + row];
+    A[e] = s.V[rr * LD + row];
   }
+  C* Rm = s.V + (size_t)LD * LD - k * cr;        // R (k x cr) in the tail of V (Q is consumed)
   __syncthreads();
-  for (int e = tid; e < k * cr; e += NT) {       // S[rr][i] = conj(X[perm[rr]][i]) -> V scratch
-    const int rr = e / cr, i = e - rr * cr;
-    s.V[e] = cconj(s.X[s.perm[rr] * LD + i]);
+  for (int e = tid; e < k * cr; e += NT) {
+    const int rr = e / cr, col = e - rr * cr;
+    Rm[e] = house_r<R, CAP>(s, rr, col);
   }
-  __syncthreads();
   const int nb = 2 * cr2;
+  __syncthreads();
   for (int e = tid; e < cr * nb; e += NT) s.X[e] = B[e];   // stage core_{c+1} (cr x 2 cr2)
   __syncthreads();
   for (int e = tid; e < k * nb; e += NT) {
     const int rr = e / nb, col = e - rr * nb;
     C acc = cmk<C>(R(0), R(0));
-    for (int i = 0; i < cr; ++i) cfma(acc, s.V[rr * cr + i], s.X[i * nb + col]);
+    for (int i = rr; i < cr; ++i) cfma(acc, Rm[rr * cr + i], s.X[i * nb + col]);   // R upper triangular
     B[e] = acc;
   }
   __syncthreads();
@@ -285,9 +365,10 @@ __device__ void shift_right(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_
   __syncthreads();
 }
 
-// centre c -> c - 1: core_c (chi_l x 2 chi_r) = L Q with Q row-isometric; L folds into core_{c-1}
+// centre c -> c - 1 (reference _shift_center_left, tt.py:125-129): core_c^H (2 chi_r x chi_l)
+// = Q R, so core_c = R^H Q^H; Q^H stays, R^H folds into core_{c-1}
 template <typename R, int CAP>
-__device__ void shift_left(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t* flag) {
+__device__ void shift_left(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int c, int32_t*) {
   using C = typename CT<R>::T;
   constexpr int LD = Scratch<R, CAP>::LD;
   constexpr int SLOT = 2 * CAP * CAP;
@@ -295,33 +376,31 @@ __device__ void shift_left(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t
   const int cl0 = dims[c - 1], cl = dims[c], cr = dims[c + 1];
   C* A = cores + (size_t)c * SLOT;
   C* P = cores + (size_t)(c - 1) * SLOT;
-  const int n = 2 * cr;                          // X = M : cl rows x n columns
+  const int n = 2 * cr;                          // X = M^H : n rows x cl columns
   for (int e = tid; e < cl * n; e += NT) {
-    const int i = e / n, j = e - i * n;
-    s.X[j * LD + i] = A[e];
+    const int i = e / n, j = e - i * n;        // M[i][j] = A flat [i * n + j]
+    s.X[i * LD + j] = cconj(A[e]);
   }
   __syncthreads();
-  jacobi<R, CAP>(s, cl, n);
-  const int r = cl < n ? cl : n;
-  rank_and_cut<R, CAP>(s, cl, n, r, false, 0.0, 0, CAP, flag);
-  const int k = s.k;
-  for (int e = tid; e < k * n; e += NT) {        // core_c[rr][col] = conj(V[perm[rr]][col])
+  const int k = house_qr<R, CAP>(s, n, cl);
+  for (int e = tid; e < k * n; e += NT) {        // core_c[rr][col] = conj(Q[col][rr])
     const int rr = e / n, col = e - rr * n;
-    A[e] = cconj(s.V[s.perm[rr] * LD + col]);
+    A[e] = cconj(s.V[rr * LD + col]);
   }
+  C* Lm = s.V + (size_t)LD * LD - cl * k;        // L = R^H (cl x k)
   __syncthreads();
-  for (int e = tid; e < cl * k; e += NT) {       // L[i][rr] = X[perm[rr]][i] -> V scratch
+  for (int e = tid; e < cl * k; e += NT) {
     const int i = e / k, rr = e - i * k;
-    s.V[e] = s.X[s.perm[rr] * LD + i];
+    Lm[e] = cconj(house_r<R, CAP>(s, rr, i));
   }
-  __syncthreads();
   const int mp = 2 * cl0;
+  __syncthreads();
   for (int e = tid; e < mp * cl; e += NT) s.X[e] = P[e];   // stage core_{c-1} (2 cl0 x cl)
   __syncthreads();
   for (int e = tid; e < mp * k; e += NT) {
     const int row = e / k, rr = e - row * k;
     C acc = cmk<C>(R(0), R(0));
-    for (int i = 0; i < cl; ++i) cfma(acc, s.X[row * cl + i], s.V[i * k + rr]);
+    for (int i = rr; i < cl; ++i) cfma(acc, s.X[row * cl + i], Lm[i * k + rr]);      // L lower triangular
     P[e] = acc;
   }
   __syncthreads();

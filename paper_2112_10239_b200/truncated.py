@@ -176,6 +176,9 @@ def simulate_terms(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=Non
                             ws.data_ptr(), ctypes.c_size_t(int(ws_bytes)), _stream())
     _lib.check(st)
     f = flags.cpu().numpy()
+    if np.any(f == 2):
+        from .errors import NotFinite
+        raise NotFinite("truncated engine produced NaN")
     if np.any(f):
         raise BondTooLarge(f"a bond exceeded the truncated engine's capacity chi={cap}; pass chi_max <= {cap}")
     vals = torch.view_as_complex(values).cpu().numpy()[:, :T]
