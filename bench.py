@@ -601,19 +601,207 @@ def run_cfg3(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- f3 (truncated TT engine)
+F3 = {"n": 500, "gates": 5000, "chi_max": 16, "eps": 0.0}   # the reference's `bench tfim` defaults
+F3_METRIC = "truncated TT simulations/sec (simulate_tt + all TFIM term values)"
+
+
+def f3_problem():
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200.hamiltonians import tfim
+    from paper_2112_10239_b200.report import tfim_workload
+
+    circuit = tfim_workload(F3["n"], F3["gates"])
+    return circuit, C.normalize_terms(tfim(F3["n"]))
+
+
+def _f3_oracle_sim(theta):
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    import oracle as O
+
+    t0 = time.perf_counter()
+    oc = O.tfim_workload_gates(F3["n"], F3["gates"])
+    tt = O.simulate_tt(oc, theta, eps=F3["eps"], chi_max=F3["chi_max"])
+    O.tt_term_values(tt, O.tfim_terms(F3["n"]))
+    return time.perf_counter() - t0
+
+
+def f3_config(batch):
+    return {"workload": "f3: reference `bench tfim` defaults, truncated TT engine (SURVEY.md row f3)",
+            "n_qubits": F3["n"], "gates": F3["gates"], "chi_max": F3["chi_max"], "eps": F3["eps"],
+            "circuit": "tfim_workload: ry+rz rows and alternating cz lines, cut to the gate count",
+            "operator": "TFIM open chain j=h=1 (all 999 term values)", "batch_per_gpu": batch,
+            "parallelism": "theta-set data parallel (one CTA per theta-set)",
+            "l2": "flushed between timed steps (256 MiB memset, untimed)"}
+
+
+def run_f3_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    from paper_2112_10239_b200.workloads import theta_sets
+
+    circuit, _ = f3_problem()
+    cores = host_cores()
+    per = cores
+    th = theta_sets(circuit.n_params, per * (args.steps + args.warmup), seed=0)
+    with mp.get_context("fork").Pool(cores) as pool:
+        for w in range(args.warmup):
+            pool.map(_f3_oracle_sim, list(th[w * per:(w + 1) * per]))
+        t0 = time.perf_counter()
+        for s_ in range(args.steps):
+            off = (args.warmup + s_) * per
+            pool.map(_f3_oracle_sim, list(th[off:off + per]))
+        wall = time.perf_counter() - t0
+    value = args.steps * per / wall
+    sample = f"{per} truncated simulations per step (oracle port of tnsim simulate_tt + expval windows)"
+    print(json.dumps({
+        "impl": "reference", "metric": F3_METRIC, "value": value, "unit": "sims/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded angles, float32-rounded)", "config": f3_config(per),
+        "cpu_baseline": {"value": value, "unit": "sims/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_f3(args):
+    """Row f3: B theta-sets of the reference's `bench tfim` workload through the truncated
+    engine per step (one tq_tt_simulate launch), complex128 like the reference."""
+    import ctypes
+
+    import torch
+
+    from paper_2112_10239_b200 import _lib, truncated as TR
+    from paper_2112_10239_b200.workloads import theta_sets
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    circuit, terms = f3_problem()
+    n, T = circuit.n_qubits, len(terms)
+    B = args.batch or torch.cuda.get_device_properties(dev).multi_processor_count
+    thetas = theta_sets(circuit.n_params, B, seed=rank)
+    table, _ = TR.compile_gates(circuit)
+    lo, hi, offs, codes = TR.term_table(terms, n)
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    d_gates, d_lo, d_hi, d_offs, d_codes = up(table.view(np.uint8)), up(lo), up(hi), up(offs), up(codes)
+    th = torch.tensor(thetas, dtype=torch.float64, device=dev)
+    values = torch.zeros(B, T, 2, dtype=torch.float64, device=dev)
+    disc = torch.zeros(B, dtype=torch.float64, device=dev)
+    norm2 = torch.zeros(B, dtype=torch.float64, device=dev)
+    bonds = torch.zeros(B, n + 1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(B, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    cap = F3["chi_max"]
+    wsb = lib.tq_tt_workspace_bytes(n, B, cap, _lib.TQ_C128)
+    wsp = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        _lib.check(lib.tq_tt_simulate(n, d_gates.data_ptr(), len(table), _lib.TQ_C128, B, th.data_ptr(), th.stride(0),
+                                      ctypes.c_double(F3["eps"]), cap, F3["chi_max"], d_lo.data_ptr(), d_hi.data_ptr(),
+                                      d_offs.data_ptr(), d_codes.data_ptr(), T, values.data_ptr(), disc.data_ptr(),
+                                      norm2.data_ptr(), bonds.data_ptr(), flags.data_ptr(), wsp.data_ptr(),
+                                      ctypes.c_size_t(int(wsb)), stream.cuda_stream))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    assert not bool(flags.any()) and bool(torch.isfinite(values).all())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.25)
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    clocks = sampler.stop() if sampler else None
+    ms = statistics.mean(times)
+    if ws > 1:
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    value = B * ws / (ms * 1e-3)
+    # e2e: host angles in, host values out, through the public entry
+    e2e_t = []
+    for i in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        TR.simulate_terms(circuit, terms, thetas, F3["eps"], F3["chi_max"], dtype="complex128")
+        e2e_t.append(time.perf_counter() - t0)
+    e2e = B * ws / statistics.mean(e2e_t[1:] if len(e2e_t) > 1 else e2e_t)
+    if rank != 0:
+        return
+    model = TR.work_model(circuit, terms, F3["chi_max"])
+    peak = ctypes.c_double(0)
+    _lib.check(lib.tq_tt_dfma_peak(2000, stream.cuda_stream, ctypes.byref(peak)))
+    achieved = model["flops"] * B / (ms * 1e-3) / 1e12
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        import multiprocessing as mp
+
+        cores = host_cores()
+        nsamp = min(cores, 16)
+        with mp.get_context("fork").Pool(nsamp) as pool:
+            t0 = time.perf_counter()
+            per = pool.map(_f3_oracle_sim, list(thetas[:nsamp]) if nsamp <= B else list(thetas))
+            wall = time.perf_counter() - t0
+        cpu = {"value": len(per) / wall, "unit": "sims/s", "cores": nsamp, "kind": "port",
+               "sample": f"{len(per)} truncated simulations, one per process (oracle port of tnsim simulate_tt "
+                         f"+ expval windows), {sum(per):.1f} CPU-s"}
+    print(json.dumps({
+        "metric": F3_METRIC, "value": value, "unit": "sims/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded angles, float32-rounded)",
+        "config": f3_config(B),
+        "roofline": {"bound": "fp64_simt", "kernel": "tt_simulate", "achieved": achieved, "peak": peak.value,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                     "peak_source": "measured DFMA probe (tq_tt_dfma_peak) on this GPU in this run",
+                     "flops_per_sim": model["flops"], "svd_flops_per_sim": model["svd_flops"],
+                     "work_model": "truncated.work_model (LAPACK-style counts; DESIGN.md section 11)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "sims/s", "h2d_bytes_per_step": int(thetas.nbytes),
+                "d2h_bytes_per_step": int(B * T * 16 + B * 8 * 2 + B * (n + 1) * 4 + B * 4)},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "results": {"max_bond": int(bonds.max()), "discarded_weight_max": float(disc.max())},
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "f3"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--segments", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     from paper_2112_10239_b200.workloads import CONFIGS
 
+    if args.config == "f3":
+        run_f3_reference(args) if args.impl == "reference" else run_f3(args)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -51,6 +51,9 @@ tq_status tq_tt_simulate(int n_qubits, const void* gates, int n_gates, int dtype
                          double* norm2, int32_t* bonds, int32_t* flags, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* Measured FP64 FMA throughput of this GPU (the roofline denominator of the complex128 path). */
+tq_status tq_tt_dfma_peak(int32_t iters, void* stream, double* tflops_out);
+
 #ifdef __cplusplus
 }
 #endif

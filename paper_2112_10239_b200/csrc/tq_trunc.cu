@@ -693,9 +693,55 @@ static WsParts ws_parts(int n, int batch, int cap, int dtype) {
   return w;
 }
 
+__global__ void dfma_probe(double* out, int iters, double seed) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) out[blockIdx.x] = r;
+}
+
 }  // namespace tqt
 
 extern "C" {
+
+tq_status tq_tt_dfma_peak(int32_t iters, void* stream, double* tflops_out) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * sms * 8) != cudaSuccess) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "cudaMalloc failed");
+    return TQ_ERR_CUDA;
+  }
+  const int blocks = sms * 8, threads = 256;
+  tqt::dfma_probe<<<blocks, threads, 0, st>>>(out, 4, 1.0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  tqt::dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 1.0);
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "%s", cudaGetErrorString(e));
+    return TQ_ERR_CUDA;
+  }
+  *tflops_out = 2.0 * 8 * 16 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+  return TQ_OK;
+}
+
 
 size_t tq_tt_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype) {
   if (n_qubits < 1 || batch < 1 || chi_cap < 1) return 0;

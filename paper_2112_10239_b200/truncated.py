@@ -183,3 +183,63 @@ def simulate_terms(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=Non
         raise BondTooLarge(f"a bond exceeded the truncated engine's capacity chi={cap}; pass chi_max <= {cap}")
     vals = torch.view_as_complex(values).cpu().numpy()[:, :T]
     return TruncatedResult(vals, disc.cpu().numpy(), bonds.cpu().numpy(), norm2.cpu().numpy())
+
+
+def work_model(circuit: Circuit, terms, chi_max) -> dict:
+    """Algorithmic real flops of one truncated simulation (eps = 0, bonds capped by chi_max),
+    by replaying the bond-dimension rules on the host:
+    - one-site gate: 4 chi_l chi_r complex MACs;
+    - centre move (Householder QR of m x n, k = min): (2 m n k - 2/3 k^3) for R plus the same
+      for Q, and k n (2 chi') for the fold into the neighbour;
+    - two-site gate: merge + gate chi_l chi_r (4 chi_m + 16), and a complex SVD of the
+      m x n block costed as a LAPACK R-SVD: 4 (4 M^2 N + 8 M N^2 + 9 N^3) real flops
+      (M >= N), the standard count a CPU reference pays;
+    - norm environments and term windows: the transfer-step GEMMs.
+    One complex MAC = 8 real flops."""
+    table, _ = compile_gates(circuit)
+    n = circuit.n_qubits
+    cap = MAX_CHI_TRUNC if chi_max is None else min(int(chi_max), MAX_CHI_TRUNC)
+    dims = [1] * (n + 1)
+    center = 0
+    cmac = 0.0
+    svd = 0.0
+
+    def move_right(c):
+        nonlocal cmac
+        m, nn = 2 * dims[c], dims[c + 1]
+        k = min(m, nn)
+        cmac += 2 * (m * nn * k - k ** 3 / 3.0) + k * nn * 2 * dims[c + 2]
+        dims[c + 1] = k
+
+    def move_left(c):
+        nonlocal cmac
+        m, nn = 2 * dims[c + 1], dims[c]
+        k = min(m, nn)
+        cmac += 2 * (m * nn * k - k ** 3 / 3.0) + 2 * dims[c - 1] * nn * k
+        dims[c] = k
+
+    for g in table:
+        site = int(g["site"])
+        if g["kind"] == 1:
+            cmac += 4 * dims[site] * dims[site + 1]
+            continue
+        while center < site:
+            move_right(center)
+            center += 1
+        while center > site:
+            move_left(center)
+            center -= 1
+        cl, cm, cr = dims[site], dims[site + 1], dims[site + 2]
+        cmac += cl * cr * (4 * cm + 16)
+        M, N = max(2 * cl, 2 * cr), min(2 * cl, 2 * cr)
+        svd += 4.0 * (4 * M * M * N + 8 * M * N * N + 9 * N ** 3)
+        dims[site + 1] = min(N, cap)
+        center = site + 1 if 2 * cl <= 2 * cr else site
+    env = sum(2 * dims[k] ** 2 * dims[k + 1] + 2 * dims[k] * dims[k + 1] ** 2 for k in range(n))
+    cmac += 2 * env
+    for _, ops in terms:
+        ops = dict(ops)
+        if ops:
+            lo, hi = min(ops), max(ops)
+            cmac += sum(2 * dims[k] ** 2 * dims[k + 1] + 2 * dims[k] * dims[k + 1] ** 2 for k in range(lo, hi + 1))
+    return {"flops": 8.0 * cmac + svd, "svd_flops": svd, "bonds": dims}
