@@ -112,7 +112,7 @@ template <typename R, int CAP>
 __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
   using C = typename CT<R>::T;
   constexpr int LD = Scratch<R, CAP>::LD;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const R tol = sizeof(R) == 8 ? R(1e-14) : R(1e-6);
   const R tiny = sizeof(R) == 8 ? R(1e-280) : R(1e-35);
   const int max_sweeps = sizeof(R) == 8 ? 40 : 20;
@@ -132,28 +132,46 @@ __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
   const R floor2 = R(fro * (sizeof(R) == 8 ? 1e-30 : 1e-13));
   if (ncols < 2) return;
   const int np = ncols + (ncols & 1);
+  // sub-warp groups: every pair of a round gets its own group when there are more pairs than
+  // warps (64 columns -> 32 pairs on 32 half-warps), so a round is one pass
+  const int sw = (np / 2 > NW) ? 16 : 32;
+  const int grp = tid / sw, gl = tid % sw, ngrp = NT / sw;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     int any = 0;
     for (int round = 0; round < np - 1; ++round) {
-      for (int pi = warp; pi < np / 2; pi += NW) {
-        int p, q;
-        if (pi == 0) { p = round; q = np - 1; }
-        else { p = (round + pi) % (np - 1); q = (round - pi + np - 1) % (np - 1); }
-        if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= ncols) continue;   // bye for an odd column count
+      for (int pi0 = 0; pi0 < np / 2; pi0 += ngrp) {   // uniform trip count: shuffles stay converged
+        const int pi = pi0 + grp;
+        int p = 0, q = 0;
+        bool live = pi < np / 2;
+        if (live) {
+          if (pi == 0) { p = round; q = np - 1; }
+          else { p = (round + pi) % (np - 1); q = (round - pi + np - 1) % (np - 1); }
+          if (p > q) { const int t = p; p = q; q = t; }
+          live = q < ncols;   // bye for an odd column count
+        }
         C* xp = s.X + p * LD;
         C* xq = s.X + q * LD;
         R a = R(0), b = R(0);
         C g = cmk<C>(R(0), R(0));
-        for (int r = lane; r < nrows; r += 32) {
-          const C u = xp[r], v = xq[r];
-          a = fma(u.x, u.x, fma(u.y, u.y, a));
-          b = fma(v.x, v.x, fma(v.y, v.y, b));
-          cfmac(g, u, v);
+        if (live) {
+          for (int r = gl; r < nrows; r += sw) {
+            const C u = xp[r], v = xq[r];
+            a = fma(u.x, u.x, fma(u.y, u.y, a));
+            b = fma(v.x, v.x, fma(v.y, v.y, b));
+            cfmac(g, u, v);
+          }
         }
-        a = warp_sum(a); b = warp_sum(b); g.x = warp_sum(g.x); g.y = warp_sum(g.y);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          if (off < sw) {
+            a += __shfl_xor_sync(0xffffffffu, a, off);
+            b += __shfl_xor_sync(0xffffffffu, b, off);
+            g.x += __shfl_xor_sync(0xffffffffu, g.x, off);
+            g.y += __shfl_xor_sync(0xffffffffu, g.y, off);
+          }
+        }
         const R ag = sqrt(g.x * g.x + g.y * g.y);
-        if (!(ag > tol * sqrt(a) * sqrt(b)) || ag < tiny || (a < floor2 && b < floor2)) continue;   // warp-uniform
+        if (!live || !(ag > tol * sqrt(a) * sqrt(b)) || ag < tiny || (a < floor2 && b < floor2)) continue;
         any = 1;
         const C e = cmk<C>(g.x / ag, g.y / ag);
         const R zeta = (b - a) / (R(2) * ag);
@@ -163,7 +181,7 @@ __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
         const R c = R(1) / sqrt(R(1) + t * t), sn = c * t;
         const C se = cmk<C>(sn * e.x, sn * e.y);          // s e
         const C sec = cmk<C>(sn * e.x, -sn * e.y);        // s conj(e)
-        for (int r = lane; r < nrows; r += 32) {
+        for (int r = gl; r < nrows; r += sw) {
           const C u = xp[r], v = xq[r];
           C nu = cmk<C>(c * u.x, c * u.y), nv = cmk<C>(c * v.x, c * v.y);
           const C m1 = cmul(sec, v), m2 = cmul(se, u);
@@ -173,7 +191,7 @@ __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
         }
         C* vp = s.V + p * LD;
         C* vq = s.V + q * LD;
-        for (int r = lane; r < ncols; r += 32) {
+        for (int r = gl; r < ncols; r += sw) {
           const C u = vp[r], v = vq[r];
           C nu = cmk<C>(c * u.x, c * u.y), nv = cmk<C>(c * v.x, c * v.y);
           const C m1 = cmul(sec, v), m2 = cmul(se, u);
