@@ -145,7 +145,10 @@ __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
         bool live = pi < np / 2;
         if (live) {
           if (pi == 0) { p = round; q = np - 1; }
-          else { p = (round + pi) % (np - 1); q = (round - pi + np - 1) % (np - 1); }
+          else {                                        // (round +- pi) mod (np - 1), no integer division
+            p = round + pi; if (p >= np - 1) p -= np - 1;
+            q = round - pi; if (q < 0) q += np - 1;
+          }
           if (p > q) { const int t = p; p = q; q = t; }
           live = q < ncols;   // bye for an odd column count
         }
@@ -170,15 +173,18 @@ __device__ void jacobi(Scratch<R, CAP>& s, int nrows, int ncols) {
             g.y += __shfl_xor_sync(0xffffffffu, g.y, off);
           }
         }
-        const R ag = sqrt(g.x * g.x + g.y * g.y);
-        if (!live || !(ag > tol * sqrt(a) * sqrt(b)) || ag < tiny || (a < floor2 && b < floor2)) continue;
+        const R ag2 = g.x * g.x + g.y * g.y;
+        // |g| <= tol sqrt(a b)  <=>  |g|^2 <= tol^2 a b  (no square roots on the convergence test)
+        if (!live || !(ag2 > tol * tol * a * b) || ag2 < tiny * tiny || (a < floor2 && b < floor2)) continue;
         any = 1;
-        const C e = cmk<C>(g.x / ag, g.y / ag);
-        const R zeta = (b - a) / (R(2) * ag);
+        const R inv = rsqrt(ag2), ag = ag2 * inv;
+        const C e = cmk<C>(g.x * inv, g.y * inv);
+        const R zeta = (b - a) * (R(0.5) * inv);
         R t;
         if (fabs(zeta) > R(1e30)) t = R(0.5) / zeta;
-        else t = (zeta >= R(0) ? R(1) : R(-1)) / (fabs(zeta) + sqrt(R(1) + zeta * zeta));
-        const R c = R(1) / sqrt(R(1) + t * t), sn = c * t;
+        else t = copysign(R(1), zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, R(1))));
+        const R c = rsqrt(fma(t, t, R(1))), sn = c * t;
+        (void)ag;
         const C se = cmk<C>(sn * e.x, sn * e.y);          // s e
         const C sec = cmk<C>(sn * e.x, -sn * e.y);        // s conj(e)
         for (int r = gl; r < nrows; r += sw) {

@@ -27,8 +27,8 @@ base = min(a for a, *_ in data)
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
 import glob
-cub = glob.glob(tmp + "/*.cubin")[0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+dis = "\n".join(subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+                for cub in sorted(glob.glob(tmp + "/*.cubin")))   # one cubin per translation unit
 # split functions
 funcs = {}
 cur = None
@@ -59,8 +59,9 @@ for l in funcs[want]:
     m = re.search(r'line (\d+)', l)
     if "## File" in l or "//## File" in l:
         m2 = re.search(r'line (\d+)', l)
+        mf = re.search(r'File "([^"]+)"', l)
         if m2:
-            curline = int(m2.group(1))
+            curline = (mf.group(1) if mf else "?", int(m2.group(1)))
         continue
     m = re.match(r"\s*/\*([0-9a-f]+)\*/", l)
     if m:
@@ -72,8 +73,22 @@ for a, src, s, ex in data:
     agg[ln][0] += s
     agg[ln][1] += ex
     tot += s
-src = open("paper_2112_10239_b200/csrc/tq_engine.cu").read().split("\n")
+srcs = {}
+
+
+def source_line(key):
+    if not key:
+        return None, "?"
+    path, ln = key
+    if not path.endswith(".cu") or not os.path.exists(path):
+        return ln, "?(other file: " + os.path.basename(path) + ")"
+    if path not in srcs:
+        srcs[path] = open(path).read().split("\n")
+    lines_ = srcs[path]
+    return ln, (lines_[ln - 1].strip()[:90] if ln <= len(lines_) else "?")
+
+
 print(f"{kname}: {tot} samples")
-for ln, (s, ex) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    text = src[ln - 1].strip()[:90] if ln and ln <= len(src) else "?(other file)"
+for key, (s, ex) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    ln, text = source_line(key)
     print(f"{100*s/tot:5.1f}%  inst={ex:>10d}  L{ln}: {text}")
