@@ -1223,7 +1223,8 @@ adj_sweep(Params p, AdjLayout A) {
   int4* sbuf = reinterpret_cast<int4*>(base + A.sbuf);
   int4* raw = reinterpret_cast<int4*>(base + A.raw);
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob) + p.c.blob_off[si];
-  for (int c = tid; c < p.c.blob_max; c += TEAM) raw[c] = blob[c];
+  blob_prefetch(raw, blob, p.c.blob_max, tid, TEAM);   // every 16-byte unit in flight at once
+  blob_wait();
   team_sync<TEAM>();
   const tq_site st = *reinterpret_cast<const tq_site*>(raw + 1);
   if (st.n_train == 0) return;   // uniform across the team
@@ -1232,21 +1233,25 @@ adj_sweep(Params p, AdjLayout A) {
   const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
   const C* gg = reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total + seg.env_base + st.g_off;
   R* gpart = reinterpret_cast<R*>(p.gpart) + (size_t)b * p.c.n_gslots + seg.gslot_begin;
-  stage_blob<R, TEAM>(raw, st, theta_b, nullptr, true, tid, mres, minfo, mps, ocode, ogidx, obase, nullptr, sbuf);
   const int cl = st.chi_l, cr = st.chi_r;
   const int lcr = 31 - __clz(cr);
   const int np = cl * cr;
   const int nops = st.op_count;
   if (TEAM == 32 && CHI <= 8 && np <= 32 && nops <= 12) {
-    team_sync<TEAM>();
+    // the core cotangent is loaded into registers before the descriptors are resolved, so
+    // its HBM/L2 latency overlaps the resolve
     const int al = tid >> lcr, be = tid & (cr - 1);
     const bool have = tid < np && !(st.pass_count && !pass_ok(p.c, st, al, be));
     const C z = cmk<C>(R(0), R(0));
+    const C g0 = have ? gg[tid] : z, g1 = have ? gg[np + tid] : z;
+    stage_blob<R, TEAM>(raw, st, theta_b, nullptr, true, tid, mres, minfo, mps, ocode, ogidx, obase, nullptr, sbuf);
+    team_sync<TEAM>();
     pair_adjoint_warp<R, 12>(nops, have ? al : 0, have ? be : 0, ocode, ogidx, mres, minfo,
                              cmk<C>(R(st.init[0]), R(st.init[1])), cmk<C>(R(st.init[2]), R(st.init[3])),
-                             have ? gg[tid] : z, have ? gg[np + tid] : z, gpart, tid);
+                             g0, g1, gpart, tid);
     return;
   }
+  stage_blob<R, TEAM>(raw, st, theta_b, nullptr, true, tid, mres, minfo, mps, ocode, ogidx, obase, nullptr, sbuf);
   for (int e = tid; e < 2 * np; e += TEAM) {
     const int sidx = e >= np, r = e - sidx * np;
     Gs[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))] = gg[e];
