@@ -51,6 +51,24 @@ tq_status tq_tt_simulate(int n_qubits, const void* gates, int n_gates, int dtype
                          double* norm2, int32_t* bonds, int32_t* flags, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* The same engine in phases, over a caller-owned device train (reference TTState, tt.py:38-76):
+ * cores [B][n][2 cap^2] complex (core k dense (chi_k, 2, chi_{k+1}) at the start of its slot),
+ * bonds [B][n+1], centers [B], discarded [B].
+ *   tq_tt_run       simulate_tt(circuit, eps, chi_max)                 tt.py:237-244
+ *   tq_tt_compress  compress(tt, eps, chi_max), in place                tt.py:299-320
+ *   tq_tt_values    per-term windows + <psi|psi>                        hamiltonians.py:129-164 */
+size_t tq_tt_state_bytes(int n_qubits, int batch, int chi_cap, int dtype);
+size_t tq_tt_values_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype);
+tq_status tq_tt_run(int n_qubits, const void* gates, int n_gates, int dtype, int batch, const void* theta,
+                    int64_t theta_stride, double eps, int chi_cap, int chi_max, void* cores, int32_t* bonds,
+                    int32_t* centers, double* discarded, int32_t* flags, void* stream);
+tq_status tq_tt_compress(int n_qubits, int dtype, int batch, double eps, int chi_cap, int chi_max, void* cores,
+                         int32_t* bonds, int32_t* centers, double* discarded, int32_t* flags, void* stream);
+tq_status tq_tt_values(int n_qubits, int dtype, int batch, int chi_cap, const void* cores, const int32_t* bonds,
+                       const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
+                       int n_terms, void* values, double* norm2, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
 /* Measured FP64 FMA throughput of this GPU (the roofline denominator of the complex128 path). */
 tq_status tq_tt_dfma_peak(int32_t iters, void* stream, double* tflops_out);
 

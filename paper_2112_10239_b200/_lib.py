@@ -91,6 +91,16 @@ def load(path: str | None = None):
         lib.tq_tt_simulate.restype = i32
         lib.tq_tt_simulate.argtypes = [i32, vp, i32, i32, i32, vp, i64, ctypes.c_double, i32, i32,
                                        vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+        lib.tq_tt_state_bytes.restype = sz
+        lib.tq_tt_state_bytes.argtypes = [i32, i32, i32, i32]
+        lib.tq_tt_values_workspace_bytes.restype = sz
+        lib.tq_tt_values_workspace_bytes.argtypes = [i32, i32, i32, i32]
+        lib.tq_tt_run.restype = i32
+        lib.tq_tt_run.argtypes = [i32, vp, i32, i32, i32, vp, i64, ctypes.c_double, i32, i32, vp, vp, vp, vp, vp, vp]
+        lib.tq_tt_compress.restype = i32
+        lib.tq_tt_compress.argtypes = [i32, i32, i32, ctypes.c_double, i32, i32, vp, vp, vp, vp, vp, vp]
+        lib.tq_tt_values.restype = i32
+        lib.tq_tt_values.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, sz, vp]
         lib.tq_tt_dfma_peak.restype = i32
         lib.tq_tt_dfma_peak.argtypes = [i32, vp, ctypes.POINTER(ctypes.c_double)]
         _lib = lib
@@ -100,7 +110,8 @@ def load(path: str | None = None):
 EXPORTED_SYMBOLS = ("tq_workspace_bytes", "tq_energy_grad", "tq_energy_grad_timed", "tq_ffma_peak",
                     "tq_term_values", "tq_inner",
                     "tq_status_string", "tq_last_error", "tq_abi_layout", "tq_build_info",
-                    "tq_tt_workspace_bytes", "tq_tt_simulate", "tq_tt_dfma_peak")
+                    "tq_tt_workspace_bytes", "tq_tt_simulate", "tq_tt_dfma_peak", "tq_tt_state_bytes",
+                    "tq_tt_values_workspace_bytes", "tq_tt_run", "tq_tt_compress", "tq_tt_values")
 
 
 def check(status: int):

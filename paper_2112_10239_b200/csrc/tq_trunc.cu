@@ -82,6 +82,7 @@ struct Params {
   double* norm2;
   int32_t* bonds;
   int32_t* flags;
+  int32_t* centers;  // [B] orthogonality centre of each train (optional)
   void* cores;     // [B][n][2 cap^2] complex
   void* envl;      // [B][n+1][cap^2]
   void* envr;      // [B][n+1][cap^2]
@@ -432,6 +433,56 @@ __device__ void shift_left(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t
   __syncthreads();
 }
 
+// compress step at site c (reference compress, tt.py:311-318): core_c (chi_l x 2 chi_r) = (U S) Vh
+// by one-sided Jacobi on its columns, truncated by (eps, chi_max) and renormalised; Vh stays,
+// U S folds into core_{c-1}
+template <typename R, int CAP>
+__device__ void truncate_left(Scratch<R, CAP>& s, const Params& p, typename CT<R>::T* cores, int32_t* dims, int c,
+                              double& disc_total, int32_t* flag) {
+  using C = typename CT<R>::T;
+  constexpr int LD = Scratch<R, CAP>::LD;
+  constexpr int SLOT = 2 * CAP * CAP;
+  const int tid = threadIdx.x;
+  const int cl0 = dims[c - 1], cl = dims[c], cr = dims[c + 1];
+  C* A = cores + (size_t)c * SLOT;
+  C* P = cores + (size_t)(c - 1) * SLOT;
+  const int n = 2 * cr;
+  for (int e = tid; e < cl * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    s.X[j * LD + i] = A[e];
+  }
+  __syncthreads();
+  jacobi<R, CAP>(s, cl, n);
+  rank_and_cut<R, CAP>(s, cl, n, cl < n ? cl : n, true, p.eps, p.chi_max, p.chi_cap, flag);
+  const int k = s.k;
+  const R sc = s.scale;
+  for (int e = tid; e < k * n; e += NT) {        // core_c[rr][col] = conj(V[perm[rr]][col])
+    const int rr = e / n, col = e - rr * n;
+    A[e] = cconj(s.V[s.perm[rr] * LD + col]);
+  }
+  C* Lm = s.V + (size_t)LD * LD - cl * k;        // (U S)[i][rr] = X[perm[rr]][i] * scale
+  __syncthreads();
+  for (int e = tid; e < cl * k; e += NT) {
+    const int i = e / k, rr = e - i * k;
+    const C x = s.X[s.perm[rr] * LD + i];
+    Lm[e] = cmk<C>(x.x * sc, x.y * sc);
+  }
+  const int mp = 2 * cl0;
+  __syncthreads();
+  for (int e = tid; e < mp * cl; e += NT) s.X[e] = P[e];
+  __syncthreads();
+  for (int e = tid; e < mp * k; e += NT) {
+    const int row = e / k, rr = e - row * k;
+    C acc = cmk<C>(R(0), R(0));
+    for (int i = 0; i < cl; ++i) cfma(acc, s.X[row * cl + i], Lm[i * k + rr]);
+    P[e] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) dims[c] = k;
+  disc_total += s.disc;
+  __syncthreads();
+}
+
 template <typename R>
 __device__ void gate_matrix(const tq_tgate& g, const R* theta_b, typename CT<R>::T* G) {
   using C = typename CT<R>::T;
@@ -584,8 +635,10 @@ __device__ void right_step(Scratch<R, CAP>& s, const typename CT<R>::T* A, int c
   __syncthreads();
 }
 
-template <typename R, int CAP>
-__global__ void __launch_bounds__(NT, 1) tt_simulate(Params p) {
+constexpr int PH_RUN = 1, PH_COMPRESS = 2, PH_VALUES = 4;
+
+template <typename R, int CAP, int PHASE>
+__global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
   using C = typename CT<R>::T;
   constexpr int SLOT = 2 * CAP * CAP;
   constexpr int ESLOT = CAP * CAP;
@@ -599,6 +652,7 @@ __global__ void __launch_bounds__(NT, 1) tt_simulate(Params p) {
   C* envr = reinterpret_cast<C*>(p.envr) + (size_t)b * (n + 1) * ESLOT;
   int32_t* dims = p.bonds + (size_t)b * (n + 1);
   int32_t* flag = p.flags + b;
+  if constexpr ((PHASE & PH_RUN) != 0) {
   const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
   // |0...0>: bond 1 everywhere
   for (int k = tid; k < n; k += NT) {
@@ -634,7 +688,19 @@ __global__ void __launch_bounds__(NT, 1) tt_simulate(Params p) {
     two_site<R, CAP>(s, p, cores, dims, site, disc, flag);
     center = m <= nn ? site + 1 : site;
   }
-  if (tid == 0) p.discarded[b] = disc;
+  if (tid == 0) { p.discarded[b] = disc; if (p.centers) p.centers[b] = center; }
+  __syncthreads();
+  }
+  if constexpr ((PHASE & PH_COMPRESS) != 0) {
+    // reference compress (tt.py:299-320): QR sweep to the right end, then truncating SVD
+    // steps back to site 0; the centre ends at 0
+    for (int c = 0; c < n - 1; ++c) shift_right<R, CAP>(s, cores, dims, c, flag);
+    double disc = 0.0;
+    for (int c = n - 1; c >= 1; --c) truncate_left<R, CAP>(s, p, cores, dims, c, disc, flag);
+    if (tid == 0) { p.discarded[b] += disc; if (p.centers) p.centers[b] = 0; }
+    __syncthreads();
+  }
+  if constexpr ((PHASE & PH_VALUES) == 0) return;
   // norm environments
   if (tid == 0) { envl[0] = cmk<C>(R(1), R(0)); envr[(size_t)n * ESLOT] = cmk<C>(R(1), R(0)); }
   __syncthreads();
@@ -683,15 +749,15 @@ __global__ void __launch_bounds__(NT, 1) tt_simulate(Params p) {
   }
 }
 
-template <typename R, int CAP>
+template <typename R, int CAP, int PHASE>
 static tq_status launch(const Params& p, cudaStream_t st) {
   const size_t smem = sizeof(Scratch<R, CAP>);
   if (smem > 227 * 1024) {
     snprintf(tq::g_err, sizeof(tq::g_err), "truncated engine: bond capacity %d needs %zu bytes of shared memory", CAP, smem);
     return TQ_ERR_UNSUPPORTED;
   }
-  cudaFuncSetAttribute(tt_simulate<R, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tt_simulate<R, CAP><<<p.batch, NT, smem, st>>>(p);
+  cudaFuncSetAttribute(tt_kernel<R, CAP, PHASE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tt_kernel<R, CAP, PHASE><<<p.batch, NT, smem, st>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(tq::g_err, sizeof(tq::g_err), "%s", cudaGetErrorString(e));
@@ -703,6 +769,41 @@ static tq_status launch(const Params& p, cudaStream_t st) {
 static int cap_bucket(int chi) { int c = 4; while (c < chi) c <<= 1; return c; }
 
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+template <int PHASE>
+static tq_status dispatch(const Params& p, int dtype, cudaStream_t st) {
+  const int c = cap_bucket(p.chi_cap);
+  if (dtype == TQ_C128) {
+    if (c <= 4) return launch<double, 4, PHASE>(p, st);
+    if (c <= 8) return launch<double, 8, PHASE>(p, st);
+    if (c <= 16) return launch<double, 16, PHASE>(p, st);
+    return launch<double, 32, PHASE>(p, st);
+  }
+  if (c <= 4) return launch<float, 4, PHASE>(p, st);
+  if (c <= 8) return launch<float, 8, PHASE>(p, st);
+  if (c <= 16) return launch<float, 16, PHASE>(p, st);
+  return launch<float, 32, PHASE>(p, st);
+}
+
+static size_t state_bytes(int n, int batch, int cap, int dtype) {
+  const size_t csz = dtype == TQ_C128 ? 16 : 8;
+  const int c = cap_bucket(cap);
+  return (size_t)batch * n * 2 * c * c * csz;
+}
+
+static size_t env_bytes(int n, int batch, int cap, int dtype) {
+  const size_t csz = dtype == TQ_C128 ? 16 : 8;
+  const int c = cap_bucket(cap);
+  return 2 * align256((size_t)batch * (n + 1) * c * c * csz);
+}
+
+static bool bad_sizes(const char* who, int n, int batch, int cap, int dtype) {
+  if (n < 1 || batch < 1 || cap < 1 || cap > 32 || (dtype != TQ_C64 && dtype != TQ_C128)) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "%s: invalid sizes (n=%d batch=%d cap=%d)", who, n, batch, cap);
+    return true;
+  }
+  return false;
+}
 
 struct WsParts { size_t cores, envl, envr, total; };
 
@@ -799,17 +900,66 @@ tq_status tq_tt_simulate(int n_qubits, const void* gates, int n_gates, int dtype
   p.cores = base + w.cores; p.envl = base + w.envl; p.envr = base + w.envr;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
-  const int c = cap_bucket(chi_cap);
-  if (dtype == TQ_C128) {
-    if (c <= 4) return launch<double, 4>(p, st);
-    if (c <= 8) return launch<double, 8>(p, st);
-    if (c <= 16) return launch<double, 16>(p, st);
-    return launch<double, 32>(p, st);
+  return dispatch<PH_RUN | PH_VALUES>(p, dtype, st);
+}
+
+size_t tq_tt_state_bytes(int n_qubits, int batch, int chi_cap, int dtype) {
+  if (n_qubits < 1 || batch < 1 || chi_cap < 1) return 0;
+  return tqt::state_bytes(n_qubits, batch, chi_cap, dtype);
+}
+
+tq_status tq_tt_run(int n_qubits, const void* gates, int n_gates, int dtype, int batch, const void* theta,
+                    int64_t theta_stride, double eps, int chi_cap, int chi_max, void* cores, int32_t* bonds,
+                    int32_t* centers, double* discarded, int32_t* flags, void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_run", n_qubits, batch, chi_cap, dtype) || n_gates < 0) return TQ_ERR_INPUT;
+  Params p{};
+  p.n = n_qubits; p.n_gates = n_gates; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max;
+  p.gates = reinterpret_cast<const tq_tgate*>(gates); p.theta = theta; p.theta_stride = theta_stride;
+  p.eps = eps; p.discarded = discarded; p.bonds = bonds; p.flags = flags; p.centers = centers; p.cores = cores;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
+  return dispatch<PH_RUN>(p, dtype, st);
+}
+
+tq_status tq_tt_compress(int n_qubits, int dtype, int batch, double eps, int chi_cap, int chi_max, void* cores,
+                         int32_t* bonds, int32_t* centers, double* discarded, int32_t* flags, void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_compress", n_qubits, batch, chi_cap, dtype)) return TQ_ERR_INPUT;
+  if (eps < 0.0 || chi_max == 0) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "tq_tt_compress: eps must be >= 0 and chi_max >= 1 (or -1)");
+    return TQ_ERR_INPUT;
   }
-  if (c <= 4) return launch<float, 4>(p, st);
-  if (c <= 8) return launch<float, 8>(p, st);
-  if (c <= 16) return launch<float, 16>(p, st);
-  return launch<float, 32>(p, st);
+  Params p{};
+  p.n = n_qubits; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max; p.eps = eps;
+  p.discarded = discarded; p.bonds = bonds; p.flags = flags; p.centers = centers; p.cores = cores;
+  return dispatch<PH_COMPRESS>(p, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t tq_tt_values_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype) {
+  if (n_qubits < 1 || batch < 1 || chi_cap < 1) return 0;
+  return tqt::env_bytes(n_qubits, batch, chi_cap, dtype);
+}
+
+tq_status tq_tt_values(int n_qubits, int dtype, int batch, int chi_cap, const void* cores, const int32_t* bonds,
+                       const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
+                       int n_terms, void* values, double* norm2, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_values", n_qubits, batch, chi_cap, dtype) || n_terms < 0) return TQ_ERR_INPUT;
+  const size_t need = env_bytes(n_qubits, batch, chi_cap, dtype);
+  if (workspace_bytes < need) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "tq_tt_values: workspace %zu < %zu bytes", workspace_bytes, need);
+    return TQ_ERR_WORKSPACE;
+  }
+  Params p{};
+  p.n = n_qubits; p.batch = batch; p.chi_cap = chi_cap; p.n_terms = n_terms;
+  p.term_lo = term_lo; p.term_hi = term_hi; p.code_off = code_off; p.codes = codes;
+  p.values = reinterpret_cast<double2*>(values); p.norm2 = norm2;
+  p.bonds = const_cast<int32_t*>(bonds); p.cores = const_cast<void*>(cores);
+  unsigned char* base = reinterpret_cast<unsigned char*>(workspace);
+  p.envl = base; p.envr = base + env_bytes(n_qubits, batch, chi_cap, dtype) / 2;
+  return dispatch<PH_VALUES>(p, dtype, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -243,3 +243,128 @@ def work_model(circuit: Circuit, terms, chi_max) -> dict:
             lo, hi = min(ops), max(ops)
             cmac += sum(2 * dims[k] ** 2 * dims[k + 1] + 2 * dims[k] * dims[k + 1] ** 2 for k in range(lo, hi + 1))
     return {"flops": 8.0 * cmac + svd, "svd_flops": svd, "bonds": dims}
+
+
+class GPUTrain:
+    """Device-resident truncated trains of a theta-set batch: the reference's ``TTState``
+    (tt.py:38-76) for B states at once.  ``cores_host(b)`` returns the reference layout
+    (chi_l, 2, chi_r) per site."""
+
+    def __init__(self, n, batch, cap, dtype, device):
+        import torch
+
+        from . import _lib
+
+        self.n, self.batch, self.cap, self.dtype, self.device = n, batch, cap, dtype, device
+        self.code = _lib.TQ_C128 if dtype == "complex128" else _lib.TQ_C64
+        lib = _lib.load()
+        self.cores = torch.zeros(int(lib.tq_tt_state_bytes(n, batch, cap, self.code)), dtype=torch.uint8, device=device)
+        self.bonds = torch.ones(batch, n + 1, dtype=torch.int32, device=device)
+        self.centers = torch.zeros(batch, dtype=torch.int32, device=device)
+        self.discarded = torch.zeros(batch, dtype=torch.float64, device=device)
+        self.flags = torch.zeros(batch, dtype=torch.int32, device=device)
+
+    def _slot(self):
+        c = 4
+        while c < self.cap:
+            c <<= 1
+        return 2 * c * c
+
+    def clone(self) -> "GPUTrain":
+        out = GPUTrain.__new__(GPUTrain)
+        out.__dict__.update(self.__dict__)
+        for k in ("cores", "bonds", "centers", "discarded", "flags"):
+            setattr(out, k, getattr(self, k).clone())
+        return out
+
+    def check(self):
+        f = self.flags.cpu().numpy()
+        if np.any(f == 2):
+            from .errors import NotFinite
+            raise NotFinite("truncated engine produced NaN")
+        if np.any(f):
+            raise BondTooLarge(f"a bond exceeded the truncated engine's capacity chi={self.cap}")
+        return self
+
+    @property
+    def bond_dims(self) -> np.ndarray:
+        return self.bonds.cpu().numpy()
+
+    def cores_host(self, b: int = 0) -> list:
+        """Cores of train b as numpy arrays (chi_l, 2, chi_r), the reference layout."""
+        import torch
+
+        cdt = torch.complex128 if self.dtype == "complex128" else torch.complex64
+        flat = self.cores.view(cdt).view(self.batch, self.n, self._slot())[b].cpu().numpy()
+        dims = self.bond_dims[b]
+        return [flat[k, : dims[k] * 2 * dims[k + 1]].reshape(dims[k], 2, dims[k + 1]).astype(complex)
+                for k in range(self.n)]
+
+    def term_values(self, terms):
+        """<P_t> per normalised term for every train: (complex [B, T], <psi|psi> [B])."""
+        import torch
+
+        from . import _lib
+        from .engine import _stream
+
+        lo, hi, offs, codes = term_table(terms, self.n)
+        dev = self.device
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        T = len(terms)
+        values = torch.zeros(self.batch, max(T, 1), 2, dtype=torch.float64, device=dev)
+        norm2 = torch.zeros(self.batch, dtype=torch.float64, device=dev)
+        lib = _lib.load()
+        wsb = int(lib.tq_tt_values_workspace_bytes(self.n, self.batch, self.cap, self.code))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        d_lo, d_hi, d_offs, d_codes = up(lo), up(hi), up(offs), up(codes)
+        _lib.check(lib.tq_tt_values(self.n, self.code, self.batch, self.cap, self.cores.data_ptr(),
+                                    self.bonds.data_ptr(), d_lo.data_ptr(), d_hi.data_ptr(), d_offs.data_ptr(),
+                                    d_codes.data_ptr(), T, values.data_ptr(), norm2.data_ptr(), ws.data_ptr(),
+                                    ctypes.c_size_t(wsb), _stream()))
+        return torch.view_as_complex(values).cpu().numpy()[:, :T], norm2.cpu().numpy()
+
+
+def simulate_train(circuit: Circuit, theta, eps: float = 0.0, chi_max=None, *, dtype: str = "complex128",
+                   device=None) -> GPUTrain:
+    """Truncated evolution of every theta-set [B, P] into device trains (reference simulate_tt)."""
+    import torch
+
+    from . import _lib
+    from .autodiff import _device
+    from .engine import _stream
+
+    cap = check_truncation_args(eps, chi_max)
+    theta = np.atleast_2d(np.asarray(theta, dtype=float))
+    if theta.shape[1] != circuit.n_params:
+        from .errors import ParamCountMismatch
+        raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
+    dev = _device(device)
+    train = GPUTrain(circuit.n_qubits, theta.shape[0], cap, dtype, dev)
+    table, _ = compile_gates(circuit)
+    d_gates = torch.from_numpy(np.ascontiguousarray(table.view(np.uint8))).to(dev)
+    th = torch.tensor(theta, dtype=torch.float64 if dtype == "complex128" else torch.float32, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.tq_tt_run(circuit.n_qubits, d_gates.data_ptr(), len(table), train.code, train.batch,
+                             th.data_ptr(), th.stride(0), ctypes.c_double(eps), cap,
+                             -1 if chi_max is None else int(chi_max), train.cores.data_ptr(), train.bonds.data_ptr(),
+                             train.centers.data_ptr(), train.discarded.data_ptr(), train.flags.data_ptr(), _stream()))
+    return train.check()
+
+
+def compress(train: GPUTrain, eps: float, chi_max=None) -> GPUTrain:
+    """Re-truncate every bond of every train (reference compress, tt.py:299-320): a new train;
+    the discarded weight accumulates onto the input's."""
+    from . import _lib
+    from .engine import _stream
+
+    check_truncation_args(eps, chi_max)
+    out = train.clone()
+    out.flags.zero_()
+    lib = _lib.load()
+    _lib.check(lib.tq_tt_compress(out.n, out.code, out.batch, ctypes.c_double(eps), out.cap,
+                                  -1 if chi_max is None else int(chi_max), out.cores.data_ptr(), out.bonds.data_ptr(),
+                                  out.centers.data_ptr(), out.discarded.data_ptr(), out.flags.data_ptr(), _stream()))
+    return out.check()

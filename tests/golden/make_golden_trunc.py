@@ -20,7 +20,7 @@ from make_golden import circ_doc, f32, ham_doc, layers_circuit, rand_circuit  # 
 from tnsim.circuits import with_params  # noqa: E402
 from tnsim.hamiltonians import PauliHamiltonian, expval, term, tfim  # noqa: E402
 from tnsim.seeding import generator  # noqa: E402
-from tnsim.tt import simulate_tt  # noqa: E402
+from tnsim.tt import compress, simulate_tt, tt_to_dense  # noqa: E402
 
 
 def case(name, circ, ham, theta, eps, chi_max):
@@ -45,8 +45,26 @@ def main():
         th = f32(rng.uniform(-np.pi, np.pi, c.n_params))
         ham = tfim(n, 0.7, 1.1) + PauliHamiltonian(n, (term(0.3, {0: "Y", 3: "X"}), term(-0.2, {1: "Z", n - 1: "Y"})))
         cases.append(case(f"random{i}", c, ham, th, (0.0, 1e-3, 1e-2, 0.0)[i], (4, None, 5, 6)[i]))
+    # compress (tt.py:299-320) of an exact / truncated train, with the dense amplitudes of
+    # the result (gauge-free) for n <= 10
+    comp = []
+    for i, (n, layers, ent, eps0, chi0, eps, chi) in enumerate([(10, 10, "cz", 0.0, None, 0.0, 4),
+                                                                (10, 12, "cnot", 0.0, 8, 1e-2, None),
+                                                                (9, 10, "cz", 0.0, None, 1e-3, 6)]):
+        c = layers_circuit(n, layers, "ry", ent)
+        th = f32(rng.uniform(-np.pi, np.pi, c.n_params))
+        tt0 = simulate_tt(with_params(c, th), eps=eps0, chi_max=chi0)
+        tt = compress(tt0, eps, chi)
+        psi = tt_to_dense(tt).amplitudes.array.reshape(-1)
+        comp.append({"name": f"compress{i}", "circuit": circ_doc(c), "ham": ham_doc(tfim(n)),
+                     "theta": [float(x) for x in th], "eps0": eps0, "chi0": chi0, "eps": eps, "chi_max": chi,
+                     "value": float(expval(tt, tfim(n))), "discarded": float(tt.discarded_weight),
+                     "bonds": [int(b) for b in tt.bond_dims], "bonds0": [int(b) for b in tt0.bond_dims],
+                     "psi_re": [float(x) for x in psi.real], "psi_im": [float(x) for x in psi.imag]})
     with open(os.path.join(HERE, "golden_trunc.json"), "w") as f:
-        json.dump({"cases": cases}, f)
+        json.dump({"cases": cases, "compress": comp}, f)
+    for c in comp:
+        print(c["name"], c["value"], c["discarded"], c["bonds"])
     for c in cases:
         print(c["name"], c["value"], c["discarded"], max(c["bonds"]))
 

@@ -85,3 +85,28 @@ def test_capacity_overflow_raises():
     terms = C.normalize_terms(tfim(14))
     with pytest.raises(BondTooLarge):
         TR.simulate_terms(c, terms, theta_sets(c.n_params, 1, seed=0), 0.0, None)
+
+
+def test_compress_and_trains_match_reference(golden_trunc):
+    for case in golden_trunc["compress"]:
+        c = to_circuit(case["circuit"])
+        h = to_ham(case["ham"], c.n_qubits)
+        terms = C.normalize_terms(h)
+        th = np.array([case["theta"]])
+        tr0 = TR.simulate_train(c, th, case["eps0"], case["chi0"])
+        assert list(tr0.bond_dims[0]) == case["bonds0"], case["name"]
+        tr = TR.compress(tr0, case["eps"], case["chi_max"])
+        assert list(tr.bond_dims[0]) == case["bonds"], case["name"]
+        assert abs(float(tr.discarded.cpu()[0]) - case["discarded"]) < 1e-10, case["name"]
+        vals, norm2 = tr.term_values(terms)
+        e = sum(cf * v for (cf, _), v in zip(terms, vals[0]))
+        assert abs(e.real - case["value"]) < 1e-10, case["name"]
+        assert abs(norm2[0] - 1.0) < 1e-10
+        cores = tr.cores_host(0)
+        psi = cores[0].reshape(2, -1)
+        for k in range(1, len(cores)):
+            psi = np.tensordot(psi, cores[k], axes=([-1], [0]))
+        ref = np.array(case["psi_re"]) + 1j * np.array(case["psi_im"])
+        np.testing.assert_allclose(psi.reshape(-1), ref, atol=1e-10, err_msg=case["name"])
+        # the input train is untouched
+        assert list(tr0.bond_dims[0]) == case["bonds0"]
