@@ -360,3 +360,72 @@ def state_inner_product(ket_circuit: Circuit, ket_theta, bra_circuit: Circuit | 
     out = E.inner_raw(db, torch.tensor(tb, dtype=tdt, device=dev), dk, torch.tensor(tk, dtype=tdt, device=dev),
                       dtype).cpu().numpy()
     return complex(out[0]) if single else out
+
+
+# --------------------------------------------------------------------------- differentiable inner product
+class InnerFunction(torch.autograd.Function):
+    """z_b = <bra(theta_bra_b)|ket(theta_ket_b)> (complex128 [B]) with exact gradients.
+
+    Every trainable gate is C + A cos(t/2) + B sin(t/2) (rx, ry, rz, crz), and z is linear in
+    each gate of either side.  Hence dz/dt = (z(t + pi) - z(t - pi)) / 4, exactly.  The
+    backward evaluates all 2P shifted angle sets of the batch in ONE tq_inner launch.  The
+    forward value is the kernel's; there is no tape (reference tt_inner, tt.py:247-255)."""
+
+    @staticmethod
+    def forward(ctx, theta_ket, theta_bra, dk, db, dtype):
+        ctx.save_for_backward(theta_ket, theta_bra)
+        ctx.dk, ctx.db, ctx.dtype = dk, db, dtype
+        return E.inner_raw(db, theta_bra.detach(), dk, theta_ket.detach(), dtype)
+
+    @staticmethod
+    def backward(ctx, gz):
+        theta_ket, theta_bra = ctx.saved_tensors
+        gk = gb = None
+
+        def shifted_grad(th, other, ket_side):
+            B, P = th.shape
+            if P == 0:
+                return torch.zeros_like(th)
+            eye = torch.eye(P, dtype=th.dtype, device=th.device) * np.pi
+            rows = torch.cat([th[:, None, :] + eye[None], th[:, None, :] - eye[None]], dim=1).reshape(B * 2 * P, P)
+            oth = other.repeat_interleave(2 * P, dim=0)
+            if ket_side:
+                z = E.inner_raw(ctx.db, oth, ctx.dk, rows, ctx.dtype)
+            else:
+                z = E.inner_raw(ctx.db, rows, ctx.dk, oth, ctx.dtype)
+            z = z.reshape(B, 2, P)
+            dz = (z[:, 0] - z[:, 1]) / 4.0
+            return (torch.conj(gz)[:, None] * dz).real.to(th.dtype)
+
+        if ctx.needs_input_grad[0]:
+            gk = shifted_grad(theta_ket.detach(), theta_bra.detach(), True)
+        if ctx.needs_input_grad[1]:
+            gb = shifted_grad(theta_bra.detach(), theta_ket.detach(), False)
+        return gk, gb, None, None, None
+
+
+def inner(ket_circuit: Circuit, theta_ket: torch.Tensor, bra_circuit: Circuit | None = None,
+          theta_bra: torch.Tensor | None = None, *, ket_init=None, bra_init=None,
+          dtype: str = "complex128") -> torch.Tensor:
+    """Torch-native, differentiable <bra|ket> (complex128 [B]) for device angle tensors
+    theta_ket [B, Pk] (and theta_bra [B, Pb]); gradients flow to both sides."""
+    n = ket_circuit.n_qubits
+    bra_circuit = bra_circuit if bra_circuit is not None else Circuit(n, (), ())
+    for circ in (ket_circuit, bra_circuit):
+        for g in circ.trainable:
+            if circ.gates[g].name not in SHIFTABLE_GATES:
+                raise UnsupportedGateForShift(f"no shift rule for gate {circ.gates[g].name!r}")
+    if theta_ket.dim() == 1:
+        theta_ket = theta_ket[None]
+    B = theta_ket.shape[0]
+    dev = theta_ket.device
+    if theta_bra is None:
+        theta_bra = torch.zeros(B, bra_circuit.n_params, dtype=theta_ket.dtype, device=dev)
+    if theta_bra.dim() == 1:
+        theta_bra = theta_bra[None]
+    if theta_bra.shape[0] == 1 and B > 1:
+        theta_bra = theta_bra.expand(B, -1)
+    tdt = E.DTYPES[dtype][1]
+    dk = E.device_plan(ket_circuit, [], "state", 1, dev, 1, init=ket_init, dtype=dtype)
+    db = E.device_plan(bra_circuit, [], "state", 1, dev, 1, init=bra_init, dtype=dtype)
+    return InnerFunction.apply(theta_ket.to(tdt), theta_bra.to(tdt), dk, db, dtype)

@@ -215,12 +215,15 @@ class TTCircuit(nn.Module):
     def forward(self, state, operator):
         return self.forward_expectation_value(state, operator)
 
-    def state_inner_product(self, state: ProductState | None, compare_state: ProductState | None) -> complex:
-        """<compare_state| U(theta) |state> (forward value)."""
-        th = self.theta().detach().double().cpu().numpy()
+    def state_inner_product(self, state: ProductState | None, compare_state: ProductState | None) -> torch.Tensor:
+        """<compare_state| U(theta) |state>: a complex scalar tensor whose gradient flows to the
+        rotation parameters (exact shift rule, one batched launch; autodiff.InnerFunction)."""
+        from .autodiff import inner
+
         ki = None if state is None else state.vectors
         bi = None if compare_state is None else compare_state.vectors
-        return _inner(self._circuit, th, None, None, ket_init=ki, bra_init=bi, dtype=self.dtype, device=self._dev())
+        th = self.theta().to(self._dev())
+        return inner(self._circuit, th, None, None, ket_init=ki, bra_init=bi, dtype=self.dtype)[0]
 
 
 # ----------------------------------------------------------------------------- operators
