@@ -395,7 +395,8 @@ def run_ours(args, cfg):
     if not args.no_cpu_baseline and ws == 1:
         cpu = cpu_baseline_block(cfg, circuit, n, host_cores())
 
-    launches_per_step = 2 + (3 if cfg.grad else 0)  # rl_sweep+reduce_energy (+ lr_sweep+adj_sweep+reduce_grad)
+    # rl_sweep + reduce_energy (+ lr_sweep + adj_sweep + reduce_grad) (+ build_wct for the fused small-chi path)
+    launches_per_step = 2 + (3 if cfg.grad else 0) + (1 if plan.chi_max <= 8 and plan.d_max <= 4 else 0)
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

@@ -95,6 +95,8 @@ struct Params {
   double* values;   // [B][n_terms][2]
   int32_t store_env;
   int32_t mode;     // 0 energy-grad, 1 values
+  const unsigned char* wct;   // per-(site, direction) bracket matrices built once per launch (or null)
+  int32_t wct_row;            // bytes per table row
 };
 
 // Optional per-stage cycle accounting (diagnostic build with -DTQ_STAGE_TIMING only).
@@ -213,7 +215,8 @@ __device__ __forceinline__ void blob_wait() { asm volatile("cp.async.wait_group 
 template <typename R, int TEAM, int DMW = 0>
 __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_row, const R* coef_row, bool rl, int tid,
                            typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
-                           SEdge<R>* sedge, int4* sbuf, typename CT<R>::T* wc = nullptr) {
+                           SEdge<R>* sedge, int4* sbuf, typename CT<R>::T* wc = nullptr,
+                           const typename CT<R>::T* wct_row = nullptr) {
   using C = typename CT<R>::T;
   constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
   constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
@@ -248,6 +251,12 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
     mres[4 * e + 0] = m00; mres[4 * e + 1] = m01; mres[4 * e + 2] = m10; mres[4 * e + 3] = m11;
     minfo[e] = ip[0];
     mps[e] = rp[FO];
+  }
+  if constexpr (DMW > 0) {
+    if (wct_row) {   // shared coefficients: the launch's table row replaces the edges entirely
+      for (int e = tid; e < 4 * DMW * DMW + 1; e += TEAM) wc[e] = wct_row[e];
+      return;
+    }
   }
   const int ec = sedge ? (rl ? st.rl_edge_count : st.lr_edge_count) : 0;
   for (int ei = tid; ei < ec; ei += TEAM) {
@@ -291,6 +300,52 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
       for (int c2 = 0; c2 < DMW * DMW; ++c2) m |= ((pm >> (2 * c2)) & 1u) << c2;
       if (tid == 0) reinterpret_cast<int*>(wc + 4 * DMW * DMW)[0] = (int)m;
     }
+  }
+}
+
+// Per-(site, direction) channel-pair bracket matrices for a launch whose coefficient row is shared
+// by every theta-set (the energy sweeps of a Hamiltonian): built once here instead of once per
+// (theta-set, site) inside the sweeps.  Warp 0: right-to-left edges, warp 1: left-to-right.
+template <typename R, int DMW>
+__global__ void __launch_bounds__(64) build_wct(Params p) {
+  using C = typename CT<R>::T;
+  constexpr int EU = sizeof(R) == 4 ? 3 : 6;
+  const int si = blockIdx.x, dir = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4* raw = reinterpret_cast<const int4*>(p.c.blob) + p.c.blob_off[si];
+  const tq_site st = *reinterpret_cast<const tq_site*>(raw + 1);
+  const bool rl = dir == 0;
+  const int4* edg = raw + 1 + SITE_UNITS + st.op_count + EU * st.lmat_count + (rl ? 0 : st.rl_edge_count);
+  const int ec = rl ? st.rl_edge_count : st.lr_edge_count;
+  const R* coef_row = reinterpret_cast<const R*>(p.coef);
+  C* out = reinterpret_cast<C*>(const_cast<unsigned char*>(p.wct) + ((size_t)si * 2 + dir) * p.wct_row);
+  C wa = cmk<C>(R(0), R(0)), wb = wa;
+  bool any = false;
+  if (lane < 2 * DMW * DMW) {
+    const int cmb = lane >> 1, sp = lane & 1;
+    const int csrc = cmb / DMW, ctgt = cmb % DMW;
+    for (int ei = 0; ei < ec; ++ei) {
+      const int4 r = edg[ei];
+      const int src = rl ? r.y : r.x, tgt = rl ? r.x : r.y;
+      if (src != csrc || tgt != ctgt) continue;
+      any = true;
+      const R cf = r.w < 0 ? R(1) : coef_row[r.w];
+      const int sidx = pauli_src<C>(r.z, sp);
+      C f = pauli_fac<C>(r.z, sp);
+      f.x *= cf; f.y *= cf;
+      const R m0 = sidx == 0 ? R(1) : R(0), m1 = R(1) - m0;
+      wa.x = fma(m0, f.x, wa.x); wa.y = fma(m0, f.y, wa.y);
+      wb.x = fma(m1, f.x, wb.x); wb.y = fma(m1, f.y, wb.y);
+    }
+    out[2 * lane + 0] = wa; out[2 * lane + 1] = wb;
+  }
+  const unsigned pm = __ballot_sync(0xffffffffu, any);
+  unsigned m = 0;
+#pragma unroll
+  for (int c2 = 0; c2 < DMW * DMW; ++c2) m |= ((pm >> (2 * c2)) & 1u) << c2;
+  if (lane == 0) {
+    C mk = cmk<C>(R(0), R(0));
+    reinterpret_cast<int*>(&mk)[0] = (int)m;
+    out[4 * DMW * DMW] = mk;
   }
 }
 
@@ -581,7 +636,19 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
     }
     return;
   }
-  const int rt = m >= 4 ? 4 : m;
+  // rows per item: minimise the critical path (rounds x rows) over the team; ties keep the
+  // taller tile (fewer operand loads).  At chi <= 8 the shapes are tiny (e.g. 3 tasks of 4x4
+  // leave 20 of 32 lanes idle with 4-row items), so the choice matters.
+  int rt = 1;
+  {
+    const int cells = ntasks * m * n;
+    int best = 1 << 30;
+    for (int r = 4; r >= 1; r >>= 1) {
+      if (r > m) continue;
+      const int cost = ((cells / r + TEAM - 1) / TEAM) * r;
+      if (cost < best) { best = cost; rt = r; }
+    }
+  }
   const int lrt = rt == 4 ? 2 : (rt == 2 ? 1 : 0);
   const int ln = 31 - __clz(n);
   const int lmb = (31 - __clz(m)) - lrt;
@@ -836,6 +903,13 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
   if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
 }
 
+// Row of the launch's bracket-matrix table for (site, direction), or null (built in the sweep).
+template <typename C>
+__device__ __forceinline__ const C* wct_row_of(const Params& p, int site, int dir) {
+  return p.wct ? reinterpret_cast<const C*>(p.wct + ((size_t)site * 2 + dir) * p.wct_row) : nullptr;
+}
+#define wct_row(p, site, dir) wct_row_of<C>(p, site, dir)
+
 // ------------------------------------------------------------------ right-to-left sweep
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
@@ -882,7 +956,8 @@ rl_sweep(Params p) {
   {
     const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
     sm.sel(0);
-    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
+    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC,
+                             wct_row(p, seg.site_begin + seg.site_count - 1, 0));
     const int nx = raw0[0].y;
     team_sync<TEAM>();
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
@@ -946,7 +1021,8 @@ rl_sweep(Params p) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].y;
       sm.sel(cur ^ 1);
-      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, true, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC,
+                               wct_row(p, seg.site_begin + q - 1, 0));
     }
     team_sync<TEAM>();
     STAGE(4);
@@ -1006,7 +1082,8 @@ lr_sweep(Params p) {
   {
     const tq_site s0 = *reinterpret_cast<const tq_site*>(raw0 + 1);
     sm.sel(0);
-    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
+    stage_blob<R, TEAM, DMW>(raw0, s0, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC,
+                             wct_row(p, seg.site_begin, 1));
     const int nx = raw0[0].z;
     team_sync<TEAM>();
     if (pf) {
@@ -1085,7 +1162,8 @@ lr_sweep(Params p) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].z;
       sm.sel(cur ^ 1);
-      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC,
+                               wct_row(p, seg.site_begin + q + 1, 1));
       sm.sel(cur);
     }
     if constexpr (MODE == 0) {
@@ -1539,7 +1617,7 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   return L;
 }
 
-struct WsLayout { size_t env, epart, gpart, total; };
+struct WsLayout { size_t env, epart, gpart, wct, wct_row, total; };
 
 static WsLayout ws_layout(const tq_chain* c, int batch, int flags, int dtype) {
   const size_t rsz = dtype == TQ_C128 ? 8 : 4;
@@ -1550,6 +1628,9 @@ static WsLayout ws_layout(const tq_chain* c, int batch, int flags, int dtype) {
   w.epart = off; off += align_up((size_t)batch * c->n_segments * 2 * rsz, 256);
   w.gpart = off;
   if (flags & TQ_FLAG_GRAD) off += align_up((size_t)batch * (c->n_gslots > 0 ? c->n_gslots : 1) * rsz, 256);
+  w.wct_row = align_up((size_t)(4 * 16 + 1) * 2 * rsz, 16);   // up to 4 channels
+  w.wct = off;
+  if (!(flags & TQ_FLAG_VALUES)) off += align_up((size_t)(c->n_sites > 0 ? c->n_sites : 1) * 2 * w.wct_row, 256);
   w.total = off + 256;
   return w;
 }
@@ -1685,7 +1766,15 @@ static tq_status energy_grad_impl(const tq_chain* c, int batch, const void* thet
   prm.c = *c; prm.batch = batch; prm.theta = theta; prm.theta_stride = ts; prm.coef = coef; prm.coef_stride = cs;
   prm.env = wb + w.env; prm.epart = wb + w.epart; prm.gpart = wb + w.gpart; prm.values = nullptr;
   prm.store_env = grad ? 1 : 0; prm.mode = 0;
+  prm.wct = nullptr; prm.wct_row = (int32_t)w.wct_row;
   if (batch == 0) return TQ_OK;
+  // one coefficient row for the whole batch + fused small-chi sweeps: build the bracket
+  // matrices once per launch instead of once per (theta-set, site)
+  if (cs == 0 && coef != nullptr && c->n_sites > 0 && chi_bucket(c->chi_max) <= 8 && c->d_max <= 4) {
+    prm.wct = wb + w.wct;
+    if (c->d_max <= 3) build_wct<R, 3><<<c->n_sites, 64, 0, s>>>(prm);
+    else build_wct<R, 4><<<c->n_sites, 64, 0, s>>>(prm);
+  }
   if (c->n_segments > 0) {
     tq_status st = dispatch<R>(prm, grad != nullptr, s);
     if (st != TQ_OK) return st;
