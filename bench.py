@@ -170,6 +170,17 @@ def cpu_oracle_rate(cfg, thetas, workers):
     return len(jobs) / wall, wall, float(sum(per))
 
 
+def _init_dist(dist, dev):
+    """NCCL, one process per GPU.  TQ_DIST_BACKEND=gloo runs the same host path with every rank
+    on the visible GPUs (a functional check of the multi-rank code on a 1-GPU box; its numbers
+    are not measurements)."""
+    backend = os.environ.get("TQ_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -232,12 +243,13 @@ def run_ours(args, cfg):
     import torch
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dist, dev)
     from paper_2112_10239_b200 import _lib, engine as E
     from paper_2112_10239_b200 import chain as C
     from paper_2112_10239_b200 import roofline
@@ -460,6 +472,7 @@ def run_cfg3(args, cfg):
     from paper_2112_10239_b200 import _lib, engine as E, roofline
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     MC, graph, circuit, rng = cfg3_problem()
@@ -680,6 +693,7 @@ def run_f3(args):
     from paper_2112_10239_b200.workloads import theta_sets
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     circuit, terms = f3_problem()
@@ -736,7 +750,7 @@ def run_f3(args):
         import torch.distributed as dist
 
         if not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=dev)
+            _init_dist(dist, dev)
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t)
