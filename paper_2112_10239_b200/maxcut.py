@@ -301,42 +301,99 @@ class MbeResult:
     seed: int
 
 
+class AdamGraph:
+    """One optimiser iteration of every restart as a replayable CUDA graph: the readout sweeps,
+    tanh loss and cotangents, the gradient sweeps, the convergence mask and the Adam/GD update,
+    all in place on device tensors.  The host only replays, and inspects the flags every
+    ``check_every`` iterations.
+
+    The semantics are those of the reference's ``minimize``, run once per restart
+    (autodiff.py:614-659):
+    - each restart freezes when its gradient norm drops below ``tol``;
+    - the final iteration evaluates without updating;
+    - the first non-finite loss or gradient raises ``DivergenceDetected`` with its iteration."""
+
+    def __init__(self, obj: MBEObjective, theta0: np.ndarray, rate: float, max_iters: int, tol: float = 1e-8,
+                 betas=(0.9, 0.999), adam_eps: float = 1e-8, optimizer: str = "adam"):
+        dev = obj.device
+        self.obj, self.rate, self.max_iters, self.tol = obj, float(rate), int(max_iters), float(tol)
+        self.b1, self.b2, self.adam_eps, self.optimizer = float(betas[0]), float(betas[1]), float(adam_eps), optimizer
+        self.theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
+        B = self.theta.shape[0]
+        self.m = torch.zeros_like(self.theta)
+        self.v = torch.zeros_like(self.theta)
+        self.active = torch.ones(B, dtype=torch.bool, device=dev)
+        self.value = torch.zeros(B, dtype=torch.float64, device=dev)
+        self.iters = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.it = torch.zeros((), dtype=torch.int64, device=dev)
+        self.bad = torch.full((), -1, dtype=torch.int64, device=dev)
+        self.graph = None
+
+    def _iteration(self):
+        o = self.obj
+        loss, grad = o(self.theta.to(o.tdt))
+        grad = grad.double()
+        finite = torch.isfinite(loss).all() & torch.isfinite(grad).all()
+        self.bad.copy_(torch.where(~finite & (self.bad < 0), self.it, self.bad))
+        self.value.copy_(torch.where(self.active, loss, self.value))
+        self.iters.copy_(torch.where(self.active, self.it.expand_as(self.iters), self.iters))
+        gnorm = torch.linalg.vector_norm(grad, dim=1)
+        self.active.copy_(self.active & (gnorm >= self.tol))
+        upd_mask = (self.active & (self.it < self.max_iters))[:, None]
+        if self.optimizer == "gd":
+            upd = self.rate * grad
+        else:
+            self.m.copy_(torch.where(upd_mask, self.b1 * self.m + (1 - self.b1) * grad, self.m))
+            self.v.copy_(torch.where(upd_mask, self.b2 * self.v + (1 - self.b2) * grad * grad, self.v))
+            step = (self.it + 1).to(torch.float64)
+            mhat = self.m / (1 - torch.pow(self.b1, step))
+            vhat = self.v / (1 - torch.pow(self.b2, step))
+            upd = self.rate * mhat / (torch.sqrt(vhat) + self.adam_eps)
+        self.theta.copy_(torch.where(upd_mask, self.theta - upd, self.theta))
+        self.it.add_(1)
+
+    def capture(self):
+        """Warm up outside the graph (plans, workspaces, kernel attributes), restore the state,
+        then capture one iteration."""
+        saved = [t.clone() for t in (self.theta, self.m, self.v, self.active, self.value, self.iters, self.it, self.bad)]
+        side = torch.cuda.Stream(device=self.obj.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._iteration()
+        torch.cuda.current_stream().wait_stream(side)
+        for t, s0 in zip((self.theta, self.m, self.v, self.active, self.value, self.iters, self.it, self.bad), saved):
+            t.copy_(s0)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self._iteration()
+        torch.cuda.synchronize()
+        return self
+
+    def run(self, check_every: int = 16):
+        if self.graph is None:
+            self.capture()
+        done = 0
+        while done < self.max_iters + 1:
+            n = min(check_every, self.max_iters + 1 - done)
+            for _ in range(n):
+                self.graph.replay()
+            done += n
+            bad = int(self.bad.item())
+            if bad >= 0:
+                raise DivergenceDetected(f"non-finite objective at iteration {bad}")
+            if not bool(self.active.any()):
+                break
+        return self.theta.cpu().numpy(), self.value.cpu().numpy(), self.iters.cpu().numpy()
+
+
 def adam_batched(obj: MBEObjective, theta0: np.ndarray, rate: float, max_iters: int, tol: float = 1e-8,
                  betas=(0.9, 0.999), adam_eps: float = 1e-8, optimizer: str = "adam"):
     """Per-restart minimise (reference autodiff.py:614-659) with restarts as the batch.
 
-    Each restart stops on its own when its gradient norm drops below ``tol``
-    (frozen thereafter), exactly like independent reference runs."""
-    dev = obj.device
-    theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
-    B = theta.shape[0]
-    m = torch.zeros_like(theta)
-    v = torch.zeros_like(theta)
-    active = torch.ones(B, dtype=torch.bool, device=dev)
-    value = torch.zeros(B, dtype=torch.float64, device=dev)
-    iters = torch.zeros(B, dtype=torch.int64, device=dev)
-    b1, b2 = betas
-    for it in range(max_iters + 1):
-        loss, grad = obj(theta.to(obj.tdt))
-        grad = grad.double()
-        if not bool(torch.isfinite(loss).all()) or not bool(torch.isfinite(grad).all()):
-            raise DivergenceDetected(f"non-finite objective at iteration {it}")
-        value = torch.where(active, loss, value)
-        iters = torch.where(active, torch.full_like(iters, it), iters)
-        gnorm = torch.linalg.vector_norm(grad, dim=1)
-        active = active & (gnorm >= tol)
-        if it == max_iters or not bool(active.any()):
-            break
-        if optimizer == "gd":
-            upd = rate * grad
-        else:
-            m = torch.where(active[:, None], b1 * m + (1 - b1) * grad, m)
-            v = torch.where(active[:, None], b2 * v + (1 - b2) * grad * grad, v)
-            mhat = m / (1 - b1 ** (it + 1))
-            vhat = v / (1 - b2 ** (it + 1))
-            upd = rate * mhat / (torch.sqrt(vhat) + adam_eps)
-        theta = torch.where(active[:, None], theta - upd, theta)
-    return theta.cpu().numpy(), value.cpu().numpy(), iters.cpu().numpy()
+    Each restart stops on its own when its gradient norm drops below ``tol`` (frozen
+    thereafter), exactly like independent reference runs.  The iterations replay one captured
+    CUDA graph (``AdamGraph``)."""
+    return AdamGraph(obj, theta0, rate, max_iters, tol, betas, adam_eps, optimizer).run()
 
 
 def solve_maxcut(graph: Graph, depth: int = 4, engine: str = "tt", eps: float = 0.0, chi_max=None,

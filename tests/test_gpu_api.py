@@ -180,3 +180,40 @@ def test_inner_product_gradients_exact():
             e[k] = h
             fd = (lossb(tk[b], tb[b] + e) - lossb(tk[b], tb[b] - e)) / (2 * h)
             assert abs(float(thb.grad[b, k]) - fd) < 1e-7, (b, k)
+
+
+def test_adam_graph_matches_eager_iterations():
+    """maxcut.AdamGraph (captured iteration, flags checked every 16 replays) against the eager
+    per-restart loop it replaces, including per-restart freezing and the final no-update step."""
+    from paper_2112_10239_b200 import maxcut as MC
+    from paper_2112_10239_b200.seeding import generator
+
+    rng = generator(7)
+    graph = MC.pairing_graph(24, 3, rng)
+    circuit = MC.brickwork_ansatz(12, 3)
+    theta0 = np.stack([rng.uniform(-np.pi, np.pi, circuit.n_params) for _ in range(4)])
+    obj = MC.MBEObjective(circuit, graph, 1.0, batch=4)
+    th_g, val_g, it_g = MC.AdamGraph(obj, theta0, 0.1, max_iters=37, tol=0.05).run(check_every=5)
+
+    dev = obj.device
+    theta = torch.tensor(theta0, dtype=torch.float64, device=dev)
+    m = torch.zeros_like(theta)
+    v = torch.zeros_like(theta)
+    active = torch.ones(4, dtype=torch.bool, device=dev)
+    value = torch.zeros(4, dtype=torch.float64, device=dev)
+    iters = torch.zeros(4, dtype=torch.int64, device=dev)
+    for it in range(38):
+        loss, grad = obj(theta.to(obj.tdt))
+        grad = grad.double()
+        value = torch.where(active, loss, value)
+        iters = torch.where(active, torch.full_like(iters, it), iters)
+        active = active & (torch.linalg.vector_norm(grad, dim=1) >= 0.05)
+        if it == 37 or not bool(active.any()):
+            break
+        m = torch.where(active[:, None], 0.9 * m + 0.1 * grad, m)
+        v = torch.where(active[:, None], 0.999 * v + 0.001 * grad * grad, v)
+        upd = 0.1 * (m / (1 - 0.9 ** (it + 1))) / (torch.sqrt(v / (1 - 0.999 ** (it + 1))) + 1e-8)
+        theta = torch.where(active[:, None], theta - upd, theta)
+    np.testing.assert_allclose(th_g, theta.cpu().numpy(), atol=1e-12)
+    np.testing.assert_allclose(val_g, value.cpu().numpy(), atol=1e-12)
+    np.testing.assert_array_equal(it_g, iters.cpu().numpy())
