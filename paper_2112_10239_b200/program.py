@@ -50,6 +50,26 @@ class ExpvalProgram:
         """Device-resident inputs -> device outputs (no host traffic)."""
         return E.energy_grad_raw(self.dp, theta_dev, self.coef, self.grad, self.dtype)
 
+    def capture(self):
+        """Capture one evaluation of ``theta_dev`` into a CUDA graph (the serving loop replays
+        it: one launch per batch instead of one per kernel).  Outputs land in the static
+        tensors ``energy`` / ``grad_dev``."""
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):           # warm-up: plan upload, workspace, kernel attributes
+            self.run_device(self.theta_dev)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self.energy, self.grad_dev = self.run_device(self.theta_dev)
+        torch.cuda.synchronize()
+        return self
+
+    def replay(self):
+        """Evaluate the current ``theta_dev`` through the captured graph."""
+        self.graph.replay()
+        return self.energy, self.grad_dev
+
     def __call__(self, theta, copy_out: bool = True):
         """theta: [batch, P] host array (numpy or pinned torch). Returns (E[B], grad[B,P] | None)."""
         if isinstance(theta, np.ndarray):
@@ -60,7 +80,7 @@ class ExpvalProgram:
         else:
             src = theta
         self.theta_dev.copy_(src, non_blocking=True)
-        energy, grad = self.run_device(self.theta_dev)
+        energy, grad = self.replay() if getattr(self, "graph", None) is not None else self.run_device(self.theta_dev)
         self.e_host.copy_(energy, non_blocking=True)
         if grad is not None:
             self.g_host.copy_(grad, non_blocking=True)
