@@ -24,6 +24,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "../../include/tq_engine.h"
 
@@ -1549,6 +1550,30 @@ static tq_status fail(tq_status s, const char* msg) {
   return s;
 }
 
+// cudaFuncSetAttribute only when a launch needs more dynamic shared memory than the kernel
+// was last opened to on this device.  The eager entry points run in loops, and re-setting the
+// attribute on every launch dominated their host cost.  The limit only ever grows (process-wide,
+// under a mutex), so concurrent callers with different plans never shrink each other's.
+static void set_smem_attr(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static const void* keys[256];
+  static size_t vals[256];
+  static int devs[256];
+  static int used = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < used; ++i)
+    if (keys[i] == fn && devs[i] == dev) {
+      if (vals[i] >= smem) return;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      vals[i] = smem;
+      return;
+    }
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (used < 256) { keys[used] = fn; devs[used] = dev; vals[used] = smem; ++used; }
+}
+
 static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 512); }
 static int chi_bucket(int chi) { int c = 2; while (c < chi) c <<= 1; return c; }
 
@@ -1679,7 +1704,7 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     q.L = make_layout(&prm.c, CHI, TEAM, sizeof(R), false, prm.mode);
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
-    cudaFuncSetAttribute(rl_sweep<R, CHI, TEAM, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED>), smem);
     if (g_timing.on) cudaEventRecord(g_timing.ev[0], s);
     rl_sweep<R, CHI, TEAM, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
     if (g_timing.on) cudaEventRecord(g_timing.ev[1], s);
@@ -1693,10 +1718,10 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
     if (g_timing.on) cudaEventRecord(g_timing.ev[2], s);
     if (prm.mode == 0) {
-      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 0, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED>), smem);
       lr_sweep<R, CHI, TEAM, 0, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
     } else {
-      cudaFuncSetAttribute(lr_sweep<R, CHI, TEAM, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 1, 0>), smem);
       lr_sweep<R, CHI, TEAM, 1, 0><<<grid, TEAM * TEAMS, smem, s>>>(q);
     }
     if (g_timing.on) cudaEventRecord(g_timing.ev[3], s);
@@ -1707,7 +1732,7 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
       const size_t asmem = (size_t)A.team_bytes * TEAMS;
       if (asmem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "adjoint shared-memory layout exceeds 227 KB");
       const int64_t units = (int64_t)prm.batch * prm.c.n_sites;
-      cudaFuncSetAttribute(adj_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem);
+      set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, TEAM>), asmem);
       if (g_timing.on) cudaEventRecord(g_timing.ev[4], s);
       adj_sweep<R, CHI, TEAM><<<(unsigned)((units + TEAMS - 1) / TEAMS), TEAM * TEAMS, asmem, s>>>(prm, A);
       if (g_timing.on) cudaEventRecord(g_timing.ev[5], s);
@@ -1833,7 +1858,7 @@ static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
   ip.team_bytes = (int32_t)align_up(off, 128);
   const size_t smem = (size_t)ip.team_bytes * TEAMS;
   if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "inner product layout exceeds shared memory");
-  cudaFuncSetAttribute(inner_sweep<R, CHI, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_smem_attr(reinterpret_cast<const void*>(inner_sweep<R, CHI, TEAM>), smem);
   inner_sweep<R, CHI, TEAM><<<(ip.batch + TEAMS - 1) / TEAMS, TEAM * TEAMS, smem, s>>>(ip);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
