@@ -98,3 +98,17 @@ def test_batch_size_and_segment_invariance():
     vs, gs = AD.grad_expval(c, h, th, dtype="complex128", segments=60)   # more segments than owned sites
     np.testing.assert_allclose(vs, vb, atol=1e-11)
     np.testing.assert_allclose(gs, gb, atol=1e-11)
+
+
+def test_values_mode_at_large_bonds():
+    """Per-term values (tq_term_values) on the unfused chi = 16 / 32 kernels against the dense
+    oracle, including multi-site and Y strings."""
+    for n, layers, dtype, tol in ((12, 16, "complex128", 1e-11), (14, 20, "complex64", 2e-5)):
+        c = layered_circuit(n, layers, "ry", "cz")
+        th = theta_sets(c.n_params, 2, seed=n)
+        groups = [{0: "Z"}, {3: "X", 4: "Y"}, {1: "Y", 6: "Z", n - 1: "X"}, {n // 2: "X", n // 2 + 1: "X"}, {}]
+        vals = AD.expectation_values(c, th, groups, dtype=dtype)
+        for b in range(2):
+            psi = O.simulate_dense(_ocirc(c), th[b])
+            ref = O.dense_term_values(psi, [(1.0, tuple(sorted(g.items()))) for g in groups])
+            np.testing.assert_allclose(vals[b], ref, atol=tol)
