@@ -22,11 +22,16 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
 
 #include "../../include/tq_engine.h"
+
+#ifndef FUSED_TC_DISABLED
+#define FUSED_TC_DISABLED 0
+#endif
 
 namespace tq {
 
@@ -68,6 +73,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
                          // folded cores (A, A2 ping-pong) and P (dense) are cp.async-prefetched
   int32_t a2;            // second folded-core buffer (direct path)
   int32_t wc;            // fused path: per-site channel-pair 2x2 bracket matrices + nonzero mask
+  int32_t tc;            // chi = 32 tensor-core path: mbarrier + TMEM base address (16 B), or -1
   int32_t team_bytes;
 };
 
@@ -96,6 +102,7 @@ struct Params {
   double* values;   // [B][n_terms][2]
   int32_t store_env;
   int32_t mode;     // 0 energy-grad, 1 values
+  int32_t use_tc;             // chi = 32 products on tcgen05 (3xTF32), see tc_product
   const unsigned char* wct;   // per-(site, direction) bracket matrices built once per launch (or null)
   int32_t wct_row;            // bytes per table row
 };
@@ -904,6 +911,119 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
   if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
 }
 
+// ------------------------------------------------------------------ tcgen05 (chi = 32, complex64)
+// N[b][s] = A[s] P[b] for all (b, s) of a 32 x 32 site as ONE real-embedded tensor-core product:
+//   D'[(s, part, i), (b, j)] = sum_{(q, k)} A'[(s, part, i), (q, k)] B'[(b, j), (q, k)]
+// with A' = [[Ar, -Ai], [Ai, Ar]] per spin (M' = 128 rows), B' = [Pr; Pi] (K' = 64), N' = 32 db.
+// 3xTF32: big*big + big*small + small*big accumulate in TMEM (fp32-level accuracy for the
+// 1e-5 parity bar).  Operands are K-major SWIZZLE_NONE core matrices (8 rows x 16 B) staged in
+// the N/BR slots, which are dead until this product's epilogue writes N.
+__device__ __forceinline__ uint32_t smem_addr_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ int kmaj_off(int row, int k) {   // floats; K' = 64: SBO = 16 core matrices
+  return (row >> 3) * 512 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(2048 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+               :: "r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_wait(uint64_t* mbar, uint32_t& phase, int tid) {
+  if (tid == 0) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" :: "r"(smem_addr_u32(mbar)));
+  asm volatile("{\n\t.reg .pred done;\n\tTQ_TC_WAIT:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+               "@!done bra TQ_TC_WAIT;\n\t}\n" :: "r"(smem_addr_u32(mbar)), "r"(phase) : "memory");
+  phase ^= 1u;
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+template <int TEAM>
+__device__ void tc_product(int tid, int db, const float2* A, const float2* P, float2* N, float* ops,
+                           uint64_t* mbar, uint32_t tmem, uint32_t& phase) {
+  constexpr int LD = 33, MS = LD * LD;
+  const int np = db * 32;          // N'
+  float* Ab = ops;                 // 128 x 64
+  float* Bb = ops + 128 * 64;      // np x 64
+  float* Bs = Bb + np * 64;        // np x 64  (make_layout reserves 128 B + 32 KB + 2 x 8 KB per channel)
+  // stage big parts of A' and B', small parts of B'.  Threads walk the destination (core-matrix)
+  // order, so the shared stores are conflict-free; the reads gather from the LD-padded sources.
+  for (int d = tid; d < 128 * 64; d += TEAM) {
+    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
+    const int sp = row >> 6, part = (row >> 5) & 1, i = row & 31, q = kq >> 5, k = kq & 31;
+    const float2 a = A[sp * MS + i * LD + k];
+    const float v = part == 0 ? (q == 0 ? a.x : -a.y) : (q == 0 ? a.y : a.x);
+    Ab[d] = tf32_rna(v);
+  }
+  for (int d = tid; d < np * 64; d += TEAM) {
+    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
+    const int bb = row >> 5, j = row & 31, q = kq >> 5, k = kq & 31;
+    const float2 pv = P[bb * MS + k * LD + j];
+    const float v = q == 0 ? pv.x : pv.y;
+    const float hb = tf32_rna(v);
+    Bb[d] = hb;
+    Bs[d] = tf32_rna(v - hb);
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  team_sync<TEAM>();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t aA = smem_addr_u32(Ab), aB = smem_addr_u32(Bb), aS = smem_addr_u32(Bs);
+  if (tid == 0) {
+#pragma unroll 1
+    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aB + ks * 256), idesc, ks > 0);
+#pragma unroll 1
+    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aS + ks * 256), idesc, 1u);
+  }
+  tc_commit_wait(mbar, phase, tid);
+  // small part of A' over the big part (its MMAs have completed)
+  for (int d = tid; d < 128 * 64; d += TEAM) {
+    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
+    const int sp = row >> 6, part = (row >> 5) & 1, i = row & 31, q = kq >> 5, k = kq & 31;
+    const float2 a = A[sp * MS + i * LD + k];
+    const float v = part == 0 ? (q == 0 ? a.x : -a.y) : (q == 0 ? a.y : a.x);
+    Ab[d] = tf32_rna(v - tf32_rna(v));
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  team_sync<TEAM>();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (tid == 0) {
+#pragma unroll 1
+    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aB + ks * 256), idesc, 1u);
+  }
+  tc_commit_wait(mbar, phase, tid);
+  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (rows (s, part, i)), columns of group w / 4
+  const int warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, sp = q >> 1, part = q & 1;
+  const int ngrp = TEAM / 128;                 // warps sharing a lane quarter
+  const int per = np / ngrp;                   // columns per warp (multiple of 8)
+  const int c0 = (warp >> 2) * per;
+  for (int cc = 0; cc < per; cc += 8) {
+    uint32_t v[8];
+    const uint32_t addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c0 + cc);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = c0 + cc + t, bb = c >> 5, j = c & 31;
+      float* dst = reinterpret_cast<float*>(N + (bb * 2 + sp) * MS + lane * LD + j);
+      dst[part] = __uint_as_float(v[t]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+
 // Row of the launch's bracket-matrix table for (site, direction), or null (built in the sweep).
 template <typename C>
 __device__ __forceinline__ const C* wct_row_of(const Params& p, int site, int dir) {
@@ -963,6 +1083,28 @@ rl_sweep(Params p) {
     team_sync<TEAM>();
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
   }
+  // chi = 32 complex64: the A[s] P[b] products run on tcgen05 (one CTA = one team)
+  constexpr bool TCK = CHI == 32 && sizeof(R) == 4 && TEAM == 512 && !FUSED_TC_DISABLED;
+  const bool use_tc = TCK && p.use_tc && p.L.tc >= 0;
+  uint64_t* tc_mbar = nullptr;
+  uint32_t tc_tmem = 0, tc_phase = 0;
+  if constexpr (TCK) {
+    if (use_tc) {
+      unsigned char* tcb = smem_raw + p.L.tc;
+      tc_mbar = reinterpret_cast<uint64_t*>(tcb);
+      uint32_t* tslot = reinterpret_cast<uint32_t*>(tcb + 8);
+      if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                     :: "r"(smem_addr_u32(tslot)), "n"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+      }
+      if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_addr_u32(tc_mbar)));
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      team_sync<TEAM>();
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      tc_tmem = *tslot;
+    }
+  }
   int cur = 0;
   for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
     team_sync<TEAM>();
@@ -992,10 +1134,42 @@ rl_sweep(Params p) {
       STAGE(2);
     } else {
       // N[b][s] = A[s] * P[b]
-      gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-          [&](int t, int) { return sm.A + (t & 1) * MS; },
-          [&](int t, int) { return PIN + (t >> 1) * MS; },
-          [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+      bool done_tc = false;
+      if constexpr (TCK) {
+        if (use_tc && cl == 32 && cr == 32 && p.use_tc != 2) {
+          float* ops = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(N) + 127) & ~uintptr_t(127));
+          tc_product<TEAM>(tid, db, reinterpret_cast<const float2*>(sm.A), reinterpret_cast<const float2*>(PIN),
+                           reinterpret_cast<float2*>(N), ops, tc_mbar, tc_tmem, tc_phase);
+          done_tc = true;
+#ifdef TQ_TC_CHECK
+          team_sync<TEAM>();
+          gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+              [&](int t, int) { return sm.A + (t & 1) * MS; },
+              [&](int t, int) { return PIN + (t >> 1) * MS; },
+              [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(sm.BR + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+          team_sync<TEAM>();
+          for (int e = tid; e < db * 2 * 1024; e += TEAM) {
+            const int t = e >> 10, i = (e >> 5) & 31, j = e & 31;
+            const C x = N[t * MS + i * LD + j], y = sm.BR[t * MS + i * LD + j];
+            if (fabsf(x.x - y.x) + fabsf(x.y - y.y) > 1e-5f)
+              printf("TCCHK blk=%d site q=%d db=%d t=%d i=%d j=%d tc=(%g,%g) simt=(%g,%g)\n", (int)blockIdx.x, q, db, t, i, j, x.x, x.y, y.x, y.y);
+          }
+          if (p.use_tc == 3) {
+            gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+                [&](int t, int) { return sm.A + (t & 1) * MS; },
+                [&](int t, int) { return PIN + (t >> 1) * MS; },
+                [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+            team_sync<TEAM>();
+          }
+          team_sync<TEAM>();
+#endif
+        }
+      }
+      if (!done_tc)
+        gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+            [&](int t, int) { return sm.A + (t & 1) * MS; },
+            [&](int t, int) { return PIN + (t >> 1) * MS; },
+            [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
       bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
@@ -1030,6 +1204,13 @@ rl_sweep(Params p) {
     if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
   }
   if (tid == 0) reinterpret_cast<C*>(p.epart)[(size_t)b * S + g] = PIN[0];
+  if constexpr (TCK) {
+    if (use_tc) {
+      team_sync<TEAM>();
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tc_tmem), "n"(128));
+    }
+  }
   STAGE_END(0);
 }
 
@@ -1574,6 +1755,19 @@ static void set_smem_attr(const void* fn, size_t smem) {
   if (used < 256) { keys[used] = fn; devs[used] = dev; vals[used] = smem; ++used; }
 }
 
+// chi = 32 complex64 products on tcgen05 (tc_product): opt-in with TQ_TC=1.  Correct (the GPU
+// parity suite passes with it on) but not yet faster: restaging the operands into the UMMA
+// layout with the 3xTF32 split costs as much as the FFMA product it replaces (cfg4 RL 10.7 vs
+// 9.7 ms).  The producers (fold, P epilogue) must emit UMMA-layout operands directly.
+static int tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TQ_TC");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 512); }
 static int chi_bucket(int chi) { int c = 2; while (c < chi) c <<= 1; return c; }
 
@@ -1594,6 +1788,11 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.env = (int32_t)off; off += (size_t)D * ms;       // RL: P in/out; LR: Lambda
   L.m = (int32_t)off; off += (size_t)(fused ? (lr && !L.direct ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
+  if (chi == 32 && rsz == 4 && !lr && !fused) {
+    // tcgen05 operands (tc_product) alias the N and BR slots: alignment + A' + B' big/small
+    const size_t need = 128 + (size_t)128 * 64 * 4 + (size_t)2 * 32 * D * 64 * 4;
+    if (off - (size_t)L.m < need) off = (size_t)L.m + need;
+  }
   L.pin = (int32_t)off;
   if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
   L.a2 = (int32_t)off;
@@ -1638,6 +1837,8 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
       if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + 2 * ms); L.ubuf = (int32_t)(L.lev + lev_bytes); }
     }
   }
+  L.tc = -1;
+  if (chi == 32 && rsz == 4 && !lr) { off = align_up(off, 16); L.tc = (int32_t)off; off += 16; }
   L.team_bytes = (int32_t)align_up(off, 128);
   return L;
 }
@@ -1791,6 +1992,7 @@ static tq_status energy_grad_impl(const tq_chain* c, int batch, const void* thet
   prm.c = *c; prm.batch = batch; prm.theta = theta; prm.theta_stride = ts; prm.coef = coef; prm.coef_stride = cs;
   prm.env = wb + w.env; prm.epart = wb + w.epart; prm.gpart = wb + w.gpart; prm.values = nullptr;
   prm.store_env = grad ? 1 : 0; prm.mode = 0;
+  prm.use_tc = tc_enabled();
   prm.wct = nullptr; prm.wct_row = (int32_t)w.wct_row;
   if (batch == 0) return TQ_OK;
   // one coefficient row for the whole batch + fused small-chi sweeps: build the bracket
@@ -1825,6 +2027,8 @@ static tq_status values_impl(const tq_chain* c, int batch, const void* theta, in
   prm.c = *c; prm.batch = batch; prm.theta = theta; prm.theta_stride = ts; prm.coef = nullptr; prm.coef_stride = 0;
   prm.env = wb + w.env; prm.epart = wb + w.epart; prm.gpart = nullptr; prm.values = values;
   prm.store_env = 1; prm.mode = 1;
+  prm.use_tc = tc_enabled();
+  prm.wct = nullptr; prm.wct_row = 0;
   if (batch == 0) return TQ_OK;
   const int64_t n = (int64_t)batch * c->n_terms;
   if (n > 0) fill_identity_values<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(*c, batch, values);

@@ -9,7 +9,14 @@
 #include <vector>
 #include <cuda_runtime.h>
 
-constexpr int M = 128, N = 64, K = 32;
+constexpr int M = 128;
+#ifndef PN
+#define PN 64
+#endif
+#ifndef PK
+#define PK 32
+#endif
+constexpr int N = PN, K = PK;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
