@@ -17,7 +17,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -253,7 +252,7 @@ def run_ours(args, cfg):
     from paper_2112_10239_b200 import _lib, engine as E
     from paper_2112_10239_b200 import chain as C
     from paper_2112_10239_b200 import roofline
-    from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, tfim
+    from paper_2112_10239_b200.hamiltonians import tfim
     from paper_2112_10239_b200.program import ExpvalProgram
     from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
 

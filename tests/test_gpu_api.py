@@ -11,7 +11,6 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs CUDA", allow_module_level=True)
 
 import oracle as O  # noqa: E402
-from conftest import ocircuit  # noqa: E402
 from helpers_engine import grad_ok64, to_circuit  # noqa: E402
 from paper_2112_10239_b200 import autodiff as AD  # noqa: E402
 from paper_2112_10239_b200 import maxcut as MC  # noqa: E402

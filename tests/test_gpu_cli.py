@@ -13,7 +13,6 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs CUDA", allow_module_level=True)
 
-import oracle as O  # noqa: E402
 from paper_2112_10239_b200 import cli  # noqa: E402
 from paper_2112_10239_b200.report import bench_tfim  # noqa: E402
 from paper_2112_10239_b200.errors import InputError  # noqa: E402

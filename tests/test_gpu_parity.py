@@ -12,7 +12,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected only on GPU ru
     pytest.skip("needs CUDA", allow_module_level=True)
 
 import oracle as O  # noqa: E402
-from conftest import ocircuit, oterms  # noqa: E402
+from conftest import ocircuit  # noqa: E402
 from helpers_engine import grad_ok64, to_circuit, to_ham, tol64  # noqa: E402
 from paper_2112_10239_b200 import autodiff as AD  # noqa: E402
 from paper_2112_10239_b200 import chain as C  # noqa: E402

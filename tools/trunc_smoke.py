@@ -1,5 +1,5 @@
 import sys; import os; R=os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0,R); sys.path.insert(0,os.path.join(R,"tests"))
-import numpy as np, time
+import numpy as np
 import oracle as O
 from paper_2112_10239_b200 import truncated as TR, chain as C
 from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
