@@ -224,7 +224,8 @@ template <typename R, int TEAM, int DMW = 0>
 __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_row, const R* coef_row, bool rl, int tid,
                            typename CT<R>::T* mres, int* minfo, R* mps, int* ocode, int* ogidx, int* obase,
                            SEdge<R>* sedge, int4* sbuf, typename CT<R>::T* wc = nullptr,
-                           const typename CT<R>::T* wct_row = nullptr) {
+                           const typename CT<R>::T* wct_row = nullptr, bool wct_async = false,
+                           bool th_pre_ok = false, R th_pre = R(0)) {
   using C = typename CT<R>::T;
   constexpr int EU = sizeof(R) == 4 ? 3 : 6;    // 16-byte units per factor entry
   constexpr int FO = sizeof(R) == 4 ? 2 : 1;    // first real-valued field (1/pscale) within an entry
@@ -247,7 +248,8 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
       const R* m = rp + FO + 2;
       m00 = cmk<C>(m[0], m[1]); m01 = cmk<C>(m[2], m[3]); m10 = cmk<C>(m[4], m[5]); m11 = cmk<C>(m[6], m[7]);
     } else {
-      const R t = slot >= 0 ? theta_row[slot] : rp[FO + 1];
+      // the caller may have loaded this lane's first angle ahead of time (latency off the path)
+      const R t = slot >= 0 ? ((th_pre_ok && e == tid) ? th_pre : theta_row[slot]) : rp[FO + 1];
       R sn, cs;
       if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); sn = R(sf); cs = R(cf); }
       else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); sn = R(sd); cs = R(cd); }
@@ -262,7 +264,8 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
   }
   if constexpr (DMW > 0) {
     if (wct_row) {   // shared coefficients: the launch's table row replaces the edges entirely
-      for (int e = tid; e < 4 * DMW * DMW + 1; e += TEAM) wc[e] = wct_row[e];
+      if (!wct_async)  // (else the caller cp.async-copied it already)
+        for (int e = tid; e < 4 * DMW * DMW + 1; e += TEAM) wc[e] = wct_row[e];
       return;
     }
   }
@@ -355,6 +358,18 @@ __global__ void __launch_bounds__(64) build_wct(Params p) {
     reinterpret_cast<int*>(&mk)[0] = (int)m;
     out[4 * DMW * DMW] = mk;
   }
+}
+
+// Angle of entry `tid` of a site's descriptor blob, loaded early by the sweeps so its global
+// latency overlaps the current site's GEMM (stage_blob then consumes it: th_pre).
+template <typename R>
+__device__ __forceinline__ R blob_theta(const int4* raw, const tq_site& st, const R* theta_row, int tid) {
+  constexpr int EU = sizeof(R) == 4 ? 3 : 6;
+  if (tid >= st.lmat_count) return R(0);
+  const int4* ents = raw + 1 + SITE_UNITS + st.op_count;
+  const int* ip = reinterpret_cast<const int*>(ents + EU * tid);
+  const int slot = ip[1];
+  return ((ip[0] & 0xff) != 0 && slot >= 0) ? theta_row[slot] : R(0);
 }
 
 __device__ __forceinline__ bool pass_ok(const tq_chain& ch, const tq_site& st, int al, int be) {
@@ -1190,6 +1205,7 @@ rl_sweep(Params p) {
             h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
           }
         });
+    STAGE(5);
     // resolve the next site's descriptors while the GEMM above is in flight (independent work)
     int nx2 = -1;
     if (has_next) {
@@ -1288,6 +1304,8 @@ lr_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int da = st.lr_da, db = st.lr_db;
     const int npin = MODE == 0 ? st.rl_db : 1;
+    R th_pre = R(0);      // next site's first angle, requested ahead of the Lambda GEMM
+    bool wct_as = false;  // next site's bracket-matrix row already on its way (cp.async)
     C* const Acur = (pf && (q & 1)) ? abuf1 : sm.A;
     if (pf) {
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // A(q) landed (P(q) may still be in flight)
@@ -1318,8 +1336,16 @@ lr_sweep(Params p) {
         const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
         async_core<C, LD, TEAM>((q & 1) ? sm.A : abuf1, env_g + sn.a_off, sn.chi_l, sn.chi_r,
                                 31 - __clz(sn.chi_r), tid);
+        if constexpr (DMW > 0) {   // and its bracket-matrix row (WC is dead after this site's bracket)
+          const C* wr = wct_row(p, seg.site_begin + q + 1, 1);
+          if (wr) {
+            for (int e = tid; e < 4 * DMW * DMW + 1; e += TEAM) async_elem(WC + e, wr + e);
+            wct_as = true;
+          }
+        }
         async_commit();
       }
+      if (has_next) th_pre = blob_theta<R>(raw0, *reinterpret_cast<const tq_site*>(raw0 + 1), theta_b, tid);
       STAGE(2);
     } else {
       // M[a][s] = Lam[a] * A[s]
@@ -1345,7 +1371,7 @@ lr_sweep(Params p) {
       nx2 = raw0[0].z;
       sm.sel(cur ^ 1);
       stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, tid, sm.mres, sm.minfo, sm.mps, sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC,
-                               wct_row(p, seg.site_begin + q + 1, 1));
+                               wct_row(p, seg.site_begin + q + 1, 1), wct_as, has_next && FUSE && MODE == 0, th_pre);
       sm.sel(cur);
     }
     if constexpr (MODE == 0) {

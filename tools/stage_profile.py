@@ -38,7 +38,7 @@ plan = prog.plan
 items = B * plan.n_segments
 sites = B * int(plan.info["sub_chain_sites"])
 print(f"{name} B={B} segments={plan.n_segments} sub-chain sites={plan.info['sub_chain_sites']} chi={plan.chi_max}")
-rl = ["stage", "fold", "N gemm", "bracket", "P gemm"]
+rl = ["stage", "fold", "N gemm", "bracket", "resolve+sync", "P gemm"]
 lr = ["stage+PIN+A", "-", "M gemm", "bracket", "Lam+G gemm", "G store", "-", "values MR", "values dots", "values fin"]
 for k, names in ((0, rl), (1, lr)):
     tot = sum(buf[16 * k + i] for i in range(16))
