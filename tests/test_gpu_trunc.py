@@ -110,3 +110,33 @@ def test_compress_and_trains_match_reference(golden_trunc):
         np.testing.assert_allclose(psi.reshape(-1), ref, atol=1e-10, err_msg=case["name"])
         # the input train is untouched
         assert list(tr0.bond_dims[0]) == case["bonds0"]
+
+
+def test_truncated_edge_cases():
+    from paper_2112_10239_b200.circuits import Circuit, standard_gate
+    from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, term
+
+    # one qubit, one-site gates only
+    c = Circuit(1, (standard_gate("ry", (0,), 0.0), standard_gate("rz", (0,), 0.0)), (0, 1))
+    h = PauliHamiltonian(1, (term(0.5, {0: "X"}), term(-1.0, {0: "Z"}), term(2.0, {})))
+    terms = C.normalize_terms(h)
+    th = np.array([[0.7, -0.3]])
+    res = TR.simulate_terms(c, terms, th, 1e-3, 4)
+    ov, _ = O.grad_expval_tt(_ocirc(c), [(t.coeff, tuple(t.ops)) for t in h.terms], th[0])
+    assert abs(res.energy([t[0] for t in terms])[0].real - ov) < 1e-12
+    assert list(res.bonds[0]) == [1, 1] and res.discarded[0] == 0.0
+    # no gates at all: |0...0>, <Z_k> = 1, <X_k> = 0, identity term = 1 (reference convention)
+    c0 = Circuit(5, (), ())
+    h0 = PauliHamiltonian(5, (term(1.0, {2: "Z"}), term(1.0, {3: "X"}), term(1.0, {})))
+    r0 = TR.simulate_terms(c0, C.normalize_terms(h0), np.zeros((2, 0)), 0.0, None)
+    np.testing.assert_allclose(r0.values, [[1, 0, 1], [1, 0, 1]], atol=1e-14)
+    np.testing.assert_allclose(r0.norm2, 1.0, atol=1e-14)
+    # complex64 trains and compress keep the reference's bonds
+    c2 = layered_circuit(10, 10, "ry", "cz")
+    t2 = theta_sets(c2.n_params, 2, seed=3)
+    tr = TR.simulate_train(c2, t2, 0.0, None, dtype="complex64")
+    comp = TR.compress(tr, 1e-2, 4)
+    assert comp.bond_dims.max() <= 4 and np.all(comp.discarded.cpu().numpy() >= 0)
+    for b in range(2):
+        tt = O.simulate_tt(_ocirc(c2), t2[b], eps=0.0, chi_max=None)
+        assert list(tr.bond_dims[b]) == list(tt.bonds)
