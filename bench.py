@@ -815,13 +815,20 @@ def run_f3(args):
         cpu = {"value": len(per) / wall, "unit": "sims/s", "cores": nsamp, "kind": "port",
                "sample": f"{len(per)} truncated simulations, one per process (oracle port of tnsim simulate_tt "
                          f"+ expval windows), {sum(per):.1f} CPU-s"}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("f3", {}).get("tt_kernel")
+        except Exception:
+            traffic = None
     print(json.dumps({
         "metric": F3_METRIC, "value": value, "unit": "sims/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded angles, float32-rounded)",
         "config": f3_config(B),
-        "roofline": {"bound": "fp64_simt", "kernel": "tt_simulate", "achieved": achieved, "peak": peak.value,
-                     "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None, "traffic": None,
+        "roofline": {"bound": "fp64_simt", "kernel": "tt_kernel", "achieved": achieved, "peak": peak.value,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None, "traffic": traffic,
                      "peak_source": "measured DFMA probe (tq_tt_dfma_peak) on this GPU in this run",
                      "flops_per_sim": model["flops"], "svd_flops_per_sim": model["svd_flops"],
                      "work_model": "truncated.work_model (LAPACK-style counts; DESIGN.md section 11)"},

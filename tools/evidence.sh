@@ -28,5 +28,5 @@ cap cfg2 rl_sweep rl_cfg2
 cap cfg2 lr_sweep lr_cfg2
 cap cfg2 adj_sweep adj_cfg2
 cap cfg4 lr_sweep lr_cfg4
-cap f3 tt_simulate tt_f3
+cap f3 tt_kernel tt_f3
 ls -la gpurun_out/ev
