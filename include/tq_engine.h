@@ -125,7 +125,10 @@ size_t tq_workspace_bytes(const tq_chain* chain, int32_t batch, int32_t flags, i
 
 /* E_b = sum_t coef[b,t] <psi(theta_b)|P_t|psi(theta_b)> (+ e_const) and, if grad != NULL,
  * grad[b,:] = dRe(E_b)/dtheta_b.  theta: [B, n_params] (row stride theta_stride elements);
- * coef: [B or 1, n_terms] real (row stride coef_stride, 0 = shared); energy: [B,2] float64. */
+ * coef: [B or 1, n_terms] real (row stride coef_stride, 0 = shared); energy: [B,2] float64.
+ * energy and grad are written once, coalesced, by the final reduction kernels: they may be
+ * device memory or pinned host memory (cudaHostAlloc; the same pointer under UVA), which
+ * returns the results to the host without a separate copy. */
 tq_status tq_energy_grad(const tq_chain* chain, int32_t dtype, int32_t batch,
                          const void* theta, int64_t theta_stride,
                          const void* coef, int64_t coef_stride,

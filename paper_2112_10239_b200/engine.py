@@ -79,8 +79,13 @@ def device_plan(circuit, terms, mode: str, batch: int, device, segments=None, in
     return dp
 
 
-def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor, want_grad: bool, dtype: str):
-    """theta [B,P], coef [B or 1, T] on the plan's device -> (E [B,2] float64, grad [B,P] | None)."""
+def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor, want_grad: bool, dtype: str,
+                    out=None):
+    """theta [B,P], coef [B or 1, T] on the plan's device -> (E [B,2] float64, grad [B,P] | None).
+
+    ``out = (energy, grad)`` supplies the output buffers instead: device tensors, or pinned host
+    tensors, which the reduction kernels then write directly over the bus (the serving
+    program's host-buffer graph uses this in place of separate device-to-host copies)."""
     code, tdt = _dtype(dtype)
     theta = theta.to(device=dp.device, dtype=tdt).contiguous()
     coef = coef.to(device=dp.device, dtype=tdt).contiguous()
@@ -89,8 +94,20 @@ def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor
         raise InputError(f"theta must be [B, {dp.plan.n_params}], got {tuple(theta.shape)}")
     if coef.shape[-1] != dp.plan.n_terms or coef.shape[0] not in (1, B):
         raise InputError("coefficient array shape mismatch")
-    energy = torch.empty(B, 2, dtype=torch.float64, device=dp.device)
-    grad = torch.empty(B, dp.plan.n_params, dtype=tdt, device=dp.device) if want_grad else None
+    if out is None:
+        energy = torch.empty(B, 2, dtype=torch.float64, device=dp.device)
+        grad = torch.empty(B, dp.plan.n_params, dtype=tdt, device=dp.device) if want_grad else None
+    else:
+        energy, grad = out
+        for t, shape, dt in ((energy, (B, 2), torch.float64), (grad, (B, dp.plan.n_params), tdt)):
+            if t is None:
+                continue
+            if tuple(t.shape) != shape or t.dtype != dt or not t.is_contiguous():
+                raise InputError(f"output buffer must be a contiguous {dt} tensor of shape {shape}")
+            if t.device.type == "cpu" and not t.is_pinned():
+                raise InputError("host output buffers must be pinned")
+        if want_grad and grad is None:
+            raise InputError("want_grad needs a gradient output buffer")
     stream = _stream()
     ws, nbytes = dp.workspace(B, _lib.TQ_FLAG_GRAD if want_grad else 0, code, stream)
     st = _lib.load().tq_energy_grad(

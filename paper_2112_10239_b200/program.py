@@ -50,10 +50,12 @@ class ExpvalProgram:
         """Device-resident inputs -> device outputs (no host traffic)."""
         return E.energy_grad_raw(self.dp, theta_dev, self.coef, self.grad, self.dtype)
 
-    def capture(self):
+    def capture(self, io: bool = True):
         """Capture one evaluation of ``theta_dev`` into a CUDA graph (the serving loop replays
         it: one launch per batch instead of one per kernel).  Outputs land in the static
-        tensors ``energy`` / ``grad_dev``."""
+        tensors ``energy`` / ``grad_dev``.  With ``io`` a second graph also holds the pinned
+        staging copies (``theta_host`` -> device, energies and gradients -> ``e_host`` /
+        ``g_host``), so a host-buffer call is a single graph launch."""
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):           # warm-up: plan upload, workspace, kernel attributes
@@ -62,6 +64,15 @@ class ExpvalProgram:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
             self.energy, self.grad_dev = self.run_device(self.theta_dev)
+        self.io_graph = None
+        if io:
+            self.io_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.io_graph, capture_error_mode="relaxed"):
+                self.theta_dev.copy_(self.theta_host, non_blocking=True)
+                # the reduction kernels store the energies and gradients straight into the
+                # pinned host buffers (mapped, same pointer under UVA): no separate D2H copies
+                self.io_energy, self.io_grad = E.energy_grad_raw(self.dp, self.theta_dev, self.coef, self.grad,
+                                                                 self.dtype, out=(self.e_host, self.g_host))
         torch.cuda.synchronize()
         return self
 
@@ -79,11 +90,20 @@ class ExpvalProgram:
             src = self.theta_host
         else:
             src = theta
-        self.theta_dev.copy_(src, non_blocking=True)
-        energy, grad = self.replay() if getattr(self, "graph", None) is not None else self.run_device(self.theta_dev)
-        self.e_host.copy_(energy, non_blocking=True)
-        if grad is not None:
-            self.g_host.copy_(grad, non_blocking=True)
+        io_graph = getattr(self, "io_graph", None)
+        if io_graph is not None:
+            if src is not self.theta_host:
+                if tuple(src.shape) != tuple(self.theta_host.shape):
+                    raise InputError(f"theta must be {tuple(self.theta_host.shape)}")
+                self.theta_host.copy_(src)
+            io_graph.replay()   # H2D copy, the evaluation kernels, D2H copies
+            grad = self.io_grad
+        else:
+            self.theta_dev.copy_(src, non_blocking=True)
+            energy, grad = self.replay() if getattr(self, "graph", None) is not None else self.run_device(self.theta_dev)
+            self.e_host.copy_(energy, non_blocking=True)
+            if grad is not None:
+                self.g_host.copy_(grad, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         if not copy_out:
             return self.e_host, self.g_host

@@ -216,3 +216,31 @@ def test_adam_graph_matches_eager_iterations():
     np.testing.assert_allclose(th_g, theta.cpu().numpy(), atol=1e-12)
     np.testing.assert_allclose(val_g, value.cpu().numpy(), atol=1e-12)
     np.testing.assert_array_equal(it_g, iters.cpu().numpy())
+
+
+def test_expval_program_serving_paths():
+    """program.ExpvalProgram (the serving path bench.py times): eager, captured device graph
+    and the captured host-buffer graph (H2D, kernels, D2H in one launch) all give the same
+    energies and gradients as grad_expval, and repeated calls see each new batch."""
+    from paper_2112_10239_b200.program import ExpvalProgram
+
+    c, h = layered_circuit(24, 6, "ry", "cz"), tfim(24)
+    B = 16
+    th = [theta_sets(c.n_params, B, seed=s).astype(np.float32) for s in (1, 2)]
+    ref = [AD.grad_expval(c, h, t.astype(np.float64), device="cuda:0") for t in th]
+    prog = ExpvalProgram(c, h, B)
+    e, g = prog(th[0])                                    # eager
+    np.testing.assert_allclose(e, ref[0][0], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(g, ref[0][1], rtol=1e-4, atol=1e-5)
+    prog.capture()
+    for k in (0, 1, 0):
+        e, g = prog(th[k])                                # numpy input -> staging buffer -> io graph
+        np.testing.assert_allclose(e, ref[k][0], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(g, ref[k][1], rtol=1e-4, atol=1e-5)
+    pinned = torch.tensor(th[1]).pin_memory()
+    e, g = prog(pinned)                                   # foreign pinned tensor
+    np.testing.assert_allclose(e, ref[1][0], rtol=1e-5, atol=1e-5)
+    prog.theta_dev.copy_(torch.tensor(th[0], device="cuda:0"))
+    energy, grad = prog.replay()                          # device-resident path
+    np.testing.assert_allclose(energy[:, 0].double().cpu().numpy(), ref[0][0], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(grad.cpu().numpy(), ref[0][1], rtol=1e-4, atol=1e-5)
