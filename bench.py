@@ -643,8 +643,10 @@ def run_cfg3(args, cfg):
         "hbm": {"achieved_gbs": byts / (ms * 1e-3) / 1e9, "peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
                 "frac": byts / (ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), "bytes_per_step": byts},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": circuit.n_params * 4,
-                "d2h_bytes_per_step": circuit.n_params * 4 + 8, "note": "single restart through mbe_objective"},
+        "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": circuit.n_params * 8,
+                "d2h_bytes_per_step": (circuit.n_params + 1) * 8,
+                "note": "single restart through mbe_objective (float64 theta in, loss + float64 gradient out; "
+                        "captured host-buffer graph from the second call)"},
         # per step: fill_identity_values + rl/lr values sweeps, rl/lr/adj + reduce_energy/reduce_grad
         "gpu_launches": 8 * args.steps,
         "clocks": clocks,

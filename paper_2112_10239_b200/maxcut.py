@@ -32,6 +32,7 @@ from .errors import (
     DuplicateEdge,
     InputError,
     InvalidLabel,
+    ParamCountMismatch,
     ParseError,
     SelfLoop,
     SizeMismatch,
@@ -282,11 +283,45 @@ def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: st
     """fun(theta) -> (loss, grad) (reference maxcut.py:219-252), one device round trip per call."""
     _check_engine(engine)
     obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device)
+    P = circuit.n_params
+    # Host-buffer serving path: the first call runs eagerly; the second captures the whole
+    # evaluation (pinned theta -> device, readout sweeps, tanh loss, gradient sweeps, loss and
+    # gradient -> pinned host) as one CUDA graph that every later call replays.
+    st = {"calls": 0, "graph": None}
+    th_host = torch.empty(1, P, dtype=torch.float64, pin_memory=True)
+    out_host = torch.empty(1, P + 1, dtype=torch.float64, pin_memory=True)
+    th_dev = torch.empty(1, P, dtype=torch.float64, device=obj.device)
+
+    def body():
+        th_dev.copy_(th_host, non_blocking=True)
+        loss, grad = obj(th_dev.to(obj.tdt))
+        out_host.copy_(torch.cat([loss.reshape(1, 1).double(), grad.double()], dim=1), non_blocking=True)
 
     def fun(theta):
-        th = torch.tensor(np.asarray(theta, dtype=float).reshape(1, -1), dtype=obj.tdt, device=obj.device)
-        loss, grad = obj(th)
-        return float(loss[0]), grad[0].double().cpu().numpy()
+        th = np.asarray(theta, dtype=float).reshape(-1)
+        if th.shape[0] != P:
+            raise ParamCountMismatch(f"expected {P} parameters, got {th.shape[0]}")
+        if not np.all(np.isfinite(th)):
+            raise InputError("theta contains non-finite values")
+        th_host.numpy()[0] = th
+        if st["graph"] is None and st["calls"] >= 1:
+            side = torch.cuda.Stream(device=obj.device)
+            side.wait_stream(torch.cuda.current_stream(obj.device))
+            with torch.cuda.stream(side):
+                body()
+            torch.cuda.current_stream(obj.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                body()
+            st["graph"] = g
+        st["calls"] += 1
+        if st["graph"] is not None:
+            st["graph"].replay()
+        else:
+            body()
+        torch.cuda.current_stream(obj.device).synchronize()
+        out = out_host.numpy()[0].copy()
+        return float(out[0]), out[1:]
 
     return fun
 

@@ -244,3 +244,26 @@ def test_expval_program_serving_paths():
     energy, grad = prog.replay()                          # device-resident path
     np.testing.assert_allclose(energy[:, 0].double().cpu().numpy(), ref[0][0], rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(grad.cpu().numpy(), ref[0][1], rtol=1e-4, atol=1e-5)
+
+
+def test_mbe_objective_captured_calls_track_inputs(golden_small):
+    """mbe_objective's fun replays a captured graph from the second call on: every call must
+    still see its own theta (against the eager batched objective), and bad inputs raise."""
+    from paper_2112_10239_b200.errors import InputError, ParamCountMismatch
+
+    d = golden_small["mbe10"]
+    g = MC.Graph(10, tuple(tuple(e) for e in d["edges"]))
+    c = MC.brickwork_ansatz(5, d["depth"])
+    fun = MC.mbe_objective(c, g, alpha=d["alpha"], dtype="complex128")
+    obj = MC.MBEObjective(c, g, d["alpha"], dtype="complex128", device="cuda:0")
+    rng = np.random.default_rng(3)
+    for _ in range(4):
+        th = rng.uniform(-np.pi, np.pi, c.n_params)
+        loss, grad = fun(th)
+        rl, rg = obj(torch.tensor(th[None], device="cuda:0"))
+        assert abs(loss - float(rl[0])) < 1e-10
+        np.testing.assert_allclose(grad, rg[0].cpu().numpy(), atol=1e-10)
+    with pytest.raises(ParamCountMismatch):
+        fun(np.zeros(c.n_params + 1))
+    with pytest.raises(InputError):
+        fun(np.full(c.n_params, np.nan))
