@@ -18,6 +18,7 @@ on the exact engine.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -132,6 +133,43 @@ class TruncatedResult:
         return out
 
 
+_GATE_CACHE: dict = {}
+_TERM_CACHE: dict = {}
+_CACHE_MAX = 8
+
+
+def _device_gates(circuit: Circuit, dev):
+    """Compiled gate table of a (frozen) circuit on ``dev``, cached per circuit object: a
+    serving loop that evaluates one circuit at many angle batches compiles and uploads it once."""
+    import torch
+
+    key = (id(circuit), str(dev))
+    hit = _GATE_CACHE.get(key)
+    if hit is not None and hit[0]() is circuit:
+        return hit[1], hit[2]
+    table, _ = compile_gates(circuit)
+    d_gates = torch.from_numpy(np.ascontiguousarray(table.view(np.uint8))).to(dev)
+    if len(_GATE_CACHE) >= _CACHE_MAX:
+        _GATE_CACHE.pop(next(iter(_GATE_CACHE)))
+    _GATE_CACHE[key] = (weakref.ref(circuit), table, d_gates)
+    return table, d_gates
+
+
+def _device_terms(terms, n: int, dev):
+    """term_table(terms, n) uploaded to ``dev``, cached on the (hashable) normalised terms."""
+    import torch
+
+    key = (tuple(terms), n, str(dev))
+    hit = _TERM_CACHE.get(key)
+    if hit is not None:
+        return hit
+    arrs = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in term_table(terms, n))
+    if len(_TERM_CACHE) >= _CACHE_MAX:
+        _TERM_CACHE.pop(next(iter(_TERM_CACHE)))
+    _TERM_CACHE[key] = arrs
+    return arrs
+
+
 def simulate_terms(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=None, *,
                    dtype: str = "complex128", device=None) -> TruncatedResult:
     """Truncated evolution of every theta-set [B, P] and <P_t> for each normalised term."""
@@ -146,20 +184,14 @@ def simulate_terms(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=Non
         from .errors import ParamCountMismatch
         raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
     B, n = theta.shape[0], circuit.n_qubits
-    table, _ = compile_gates(circuit)
-    lo, hi, offs, codes = term_table(terms, n)
     from .autodiff import _device
 
     dev = _device(device)   # EngineUnavailable without a GPU: there is no CPU fallback
+    table, d_gates = _device_gates(circuit, dev)
+    d_lo, d_hi, d_offs, d_codes = _device_terms(terms, n, dev)
     code = _lib.TQ_C128 if dtype == "complex128" else _lib.TQ_C64
     tdt = torch.float64 if dtype == "complex128" else torch.float32
     lib = _lib.load()
-
-    def up(a):
-        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-
-    d_gates = up(table.view(np.uint8))
-    d_lo, d_hi, d_offs, d_codes = up(lo), up(hi), up(offs), up(codes)
     th = torch.tensor(theta, dtype=tdt, device=dev)
     T = len(terms)
     values = torch.zeros(B, max(T, 1), 2, dtype=torch.float64, device=dev)
@@ -343,8 +375,7 @@ def simulate_train(circuit: Circuit, theta, eps: float = 0.0, chi_max=None, *, d
         raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
     dev = _device(device)
     train = GPUTrain(circuit.n_qubits, theta.shape[0], cap, dtype, dev)
-    table, _ = compile_gates(circuit)
-    d_gates = torch.from_numpy(np.ascontiguousarray(table.view(np.uint8))).to(dev)
+    table, d_gates = _device_gates(circuit, dev)
     th = torch.tensor(theta, dtype=torch.float64 if dtype == "complex128" else torch.float32, device=dev)
     lib = _lib.load()
     _lib.check(lib.tq_tt_run(circuit.n_qubits, d_gates.data_ptr(), len(table), train.code, train.batch,
