@@ -18,7 +18,7 @@ from . import chain as C
 from .errors import BondTooLarge, EngineError, EngineUnavailable, InputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtq_engine.so")
+LIB_PATH = os.environ.get("TQ_ENGINE_LIB") or os.path.join(HERE, "libtq_engine.so")
 
 TQ_OK, TQ_ERR_INPUT, TQ_ERR_UNSUPPORTED, TQ_ERR_CUDA, TQ_ERR_WORKSPACE = 0, 1, 2, 3, 4
 TQ_C64, TQ_C128 = 0, 1

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 from paper_2112_10239_b200 import _lib  # noqa: E402
 
-lib = _lib.load(os.path.join(ROOT, "paper_2112_10239_b200", "libtq_engine_timing.so"))
+lib = _lib.load(os.environ.get("TQ_TIMING_LIB") or os.path.join(ROOT, "paper_2112_10239_b200", "libtq_engine_timing.so"))
 lib.tq_stage_cycles.restype = ctypes.c_int32
 lib.tq_stage_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
 from paper_2112_10239_b200 import engine as E  # noqa: E402
