@@ -138,8 +138,11 @@ NUMPY_SIZES = [C.SITE_DTYPE.itemsize, C.OP_DTYPE.itemsize, C.MAT_DTYPE.itemsize,
 
 
 def pack_opcode(ops: np.ndarray) -> np.ndarray:
-    """Kernel op code: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24] toff[24:29]."""
-    return (ops["lmat"] | (ops["src"] << 9) | (ops["shift"] << 11) | (ops["bits"] << 16)
+    """Kernel op code: lmat[0:9] src[9:11] kshift[11:16] bits[16:18] tidx+1[18:24] toff[24:29];
+    kshift = the digit's position in the pair key alpha | beta << 8 (csrc oc_digit)."""
+    ksh = ops["shift"] + np.where(ops["src"] == 2, 8, 0)
+    bits = np.where(ops["src"] == 0, 0, ops["bits"])
+    return (ops["lmat"] | (ops["src"] << 9) | (ksh << 11) | (bits << 16)
             | ((ops["tidx"] + 1) << 18) | (ops["toff"] << 24)).astype(np.int32)
 
 

@@ -80,14 +80,16 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
 // Site edge staged in shared memory with its coefficient already resolved for this theta-set.
 template <typename R> struct SEdge { int a, b, op; R coef; };
 
-// Packed column op: lmat[0:9] src[9:11] shift[11:16] bits[16:18] tidx+1[18:24] toff[24:29]
+// Packed column op: lmat[0:9] src[9:11] kshift[11:16] bits[16:18] tidx+1[18:24] toff[24:29].
+// kshift is the digit's bit position in the pair key al | be << 8 (shift, plus 8 when the digit
+// comes from beta), so the decode is one shift and mask; bits = 0 (no digit) gives digit 0.
 __device__ __forceinline__ int oc_lmat(int c) { return c & 511; }
 __device__ __forceinline__ int oc_tidx(int c) { return ((c >> 18) & 63) - 1; }
 __device__ __forceinline__ int oc_toff(int c) { return (c >> 24) & 31; }
 __device__ __forceinline__ int oc_bits(int c) { return (c >> 16) & 3; }
+__device__ __forceinline__ int oc_shift(int c) { return (c >> 11) & 7; }   // within al or be
 __device__ __forceinline__ int oc_digit(int c, int al, int be) {
-  const int src = (c >> 9) & 3, shift = (c >> 11) & 31, mask = (1 << ((c >> 16) & 3)) - 1;
-  return src == 0 ? 0 : (((src == 1 ? al : be) >> shift) & mask);
+  return ((al | (be << 8)) >> ((c >> 11) & 31)) & ((1 << ((c >> 16) & 3)) - 1);
 }
 
 struct Params {
@@ -165,7 +167,8 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
   }
   for (int o = tid; o < st.op_count; o += TEAM) {
     const tq_op& op = ch.ops[st.op_begin + o];
-    ocode[o] = op.lmat | (op.src << 9) | (op.shift << 11) | (op.bits << 16) | ((op.tidx + 1) << 18) | (op.toff << 24);
+    const int ksh = op.shift + (op.src == 2 ? 8 : 0);
+    ocode[o] = op.lmat | (op.src << 9) | (ksh << 11) | ((op.src ? op.bits : 0) << 16) | ((op.tidx + 1) << 18) | (op.toff << 24);
     if (op.tidx >= 0) ogidx[op.tidx] = op.gidx;   // trainable index -> partial-gradient slot
     obase[o] = op.tbase;
   }
@@ -492,7 +495,7 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
       const int bits = oc_bits(c);
       if (!bits) continue;
       const int d = (e >> oc_toff(c)) & ((1 << bits) - 1);
-      const int src = (c >> 9) & 3, shift = (c >> 11) & 31;
+      const int src = (c >> 9) & 3, shift = oc_shift(c);
       if (src == 1) al |= d << shift; else be |= d << shift;
     }
     C g0 = cmk<C>(R(0), R(0)), g1 = g0;
@@ -668,7 +671,7 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
     int best = 1 << 30;
     for (int r = 4; r >= 1; r >>= 1) {
       if (r > m) continue;
-      const int cost = ((cells / r + TEAM - 1) / TEAM) * r;
+      const int cost = (((cells >> (r >> 1)) + TEAM - 1) / TEAM) * r;
       if (cost < best) { best = cost; rt = r; }
     }
   }
