@@ -1486,8 +1486,14 @@ struct AdjLayout {
   int32_t g, mres, minfo, mps, ocode, ogidx, obase, sbuf, raw, lev, ubuf, contrib, team_bytes, tree;
 };
 
+// Min resident 128-thread adjoint CTAs per SM (team-of-32 path).  6 measured best
+// on cfg2 (adj 0.0830 -> 0.0787 ms vs 4; 8 gives 0.0814), tools/exp_variant.sh.
+// fp32 only: at 6 the fp64 CHI=8 instance spills ~500 B, so fp64 keeps 4.
+#ifndef TQ_ADJ_MINB
+#define TQ_ADJ_MINB 6
+#endif
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : 1)
 adj_sweep(Params p, AdjLayout A) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
