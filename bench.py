@@ -1,16 +1,20 @@
 #!/usr/bin/env python
 """Benchmark: TT-circuit TFIM energy+gradient evaluations per second on B200.
 
-Default workload (N=1): BASELINE.json configs[1] = cfg2: TTCircuit n=100, 10 layers
-(5 RotY rows + 5 CZ lines, reading A), TFIM energy + full gradient, 256 parameter
-sets per step.  ``--config cfg4`` (n=1000, 20 layers, chain sharded over ranks) and
-``--config cfg5`` (n=1024 per GPU, forward only, weak scaling) are also available.
+Default workload: BASELINE.json configs[3] = cfg4, the configuration the metric is quoted on
+("n qubits, L layers (1/2/4/8 B200)"): TTCircuit n=1000, 20 layers (10 RotY rows + 10 CZ
+lines, reading A), TFIM energy + full gradient, 64 parameter sets per step, the qubit chain
+sharded over the ranks (strong scaling).  ``--config cfg2`` (n=100, B=256, theta-set data
+parallel), ``cfg5`` (n=1024 per GPU, forward only, weak scaling), ``cfg1``, ``cfg3`` (MBE
+MaxCut Adam step) and ``f3`` (truncated engine) are also available.  ``--gpus N`` outside
+torchrun re-launches itself as N ranks (one per GPU, NCCL).
 
 One JSON line on rank 0 (contract in the task brief): value = whole-job evals/s from
 device-resident inputs; e2e = same metric through ExpvalProgram with pinned host
 buffers (H2D + D2H inside the timed region); roofline for the dominant sweep kernel
-against the measured FP32 FFMA peak; cpu_baseline = the CPU oracle port of the
-reference timed on this host.  ``--impl reference`` times that CPU path alone.
+with SURVEY.md section 8(d)'s work formulas against the measured FP32 FFMA peak;
+cpu_baseline = the CPU oracle port of the reference timed on this host.
+``--impl reference`` times that CPU path alone.
 """
 
 from __future__ import annotations
@@ -189,33 +193,55 @@ def host_cores() -> int:
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, cfg):
+    """The reference's CPU path (the oracle port of tnsim) on this host's cores, same metric and
+    config as our arm.  cfg1/cfg2: exact taped E+grad (grad_expval engine='tt', eps=0), one
+    theta-set per process.  cfg4: the exact taped gradient is infeasible on the reference
+    (eps=0 bond 2^lines = 1024), its exact alternative is the shift rule = 2P+1 forward
+    evaluations, so each step times one forward evaluate_expval(eps=1e-12) per process and
+    evals/s = forwards/s / (2P+1).  cfg5: forward-only, evals/s = forwards/s.  Under torchrun
+    only rank 0 runs (the others exit without work)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     from paper_2112_10239_b200.workloads import theta_sets
 
     cores = host_cores()
-    per_step = max(cores, 4)
-    thetas = theta_sets(cfg.circuit().n_params, per_step * (args.steps + args.warmup), seed=0)
+    n = cfg.n * ws if cfg.name == "cfg5" else cfg.n
+    forward = cfg.name in ("cfg4", "cfg5")
+    per_step = max(cores, 4) if not forward else cores
+    circuit = cfg.circuit() if cfg.name != "cfg5" else __import__(
+        "paper_2112_10239_b200.workloads", fromlist=["x"]).layered_circuit(n, cfg.layers, cfg.rot, cfg.ent)
+    P = circuit.n_params
+    thetas = theta_sets(P, per_step * (args.steps + args.warmup), seed=0)
     import multiprocessing as mp
 
-    jobs = [(cfg.n, cfg.layers, cfg.rot, cfg.ent, th) for th in thetas]
+    fn = _oracle_forward if forward else _oracle_eval
+    jobs = [(n, cfg.layers, cfg.rot, cfg.ent, th) for th in thetas]
     with mp.get_context("fork").Pool(cores) as pool:
         for w in range(args.warmup):
-            pool.map(_oracle_eval, jobs[w * per_step:(w + 1) * per_step])
+            pool.map(fn, jobs[w * per_step:(w + 1) * per_step])
         t0 = time.perf_counter()
         off = args.warmup * per_step
         for s in range(args.steps):
-            pool.map(_oracle_eval, jobs[off + s * per_step: off + (s + 1) * per_step])
+            pool.map(fn, jobs[off + s * per_step: off + (s + 1) * per_step])
         wall = time.perf_counter() - t0
-    value = args.steps * per_step / wall
-    sample = f"{per_step} theta-sets of {cfg.name} per step (CPU oracle port of tnsim grad_expval(engine='tt', eps=0))"
+    rate = args.steps * per_step / wall
+    if cfg.name == "cfg4":
+        value = rate / (2 * P + 1)
+        sample = (f"{per_step} forward evaluations of cfg4 per step (oracle port of tnsim evaluate_expval "
+                  f"engine='tt' eps=1e-12), {rate:.3f} forwards/s; exact E+grad = shift rule, {2 * P + 1} forwards")
+    elif cfg.name == "cfg5":
+        value = rate
+        sample = f"{per_step} forward evaluations of cfg5 n={n} per step (oracle port of tnsim evaluate_expval eps=1e-12)"
+    else:
+        value = rate
+        sample = f"{per_step} theta-sets of {cfg.name} per step (CPU oracle port of tnsim grad_expval(engine='tt', eps=0))"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic (seeded U[-pi,pi) angles, float32-rounded)",
-        "config": config_block(cfg, None, per_step),
+        "higher_is_better": True, "scaling": "strong" if cfg.name == "cfg4" else "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded U[-pi,pi) angles, float32-rounded)",
+        "config": config_block(cfg, None, cfg.batch if forward else per_step, n, ws),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -238,6 +264,19 @@ def config_block(cfg, plan, batch, n_override=None, world=1):
 
 
 # ----------------------------------------------------------------------------- our arm
+def work_model(cfg, circuit, ham, batch):
+    """SURVEY.md section 8(d) per-evaluation work (the official formulas) plus the kernels'
+    executed-cMAC model, both from the unsegmented plan of the full chain."""
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200 import roofline
+
+    terms = C.normalize_terms(ham)
+    t1 = sum(1 for _, ops in terms if len(ops) == 1)
+    t2 = sum(1 for _, ops in terms if len(ops) == 2)
+    plan1 = C.compile_chain(circuit, terms, "energy", batch=batch, segments=1)
+    return roofline.survey_model(plan1, t1, t2, cfg.layers, cfg.grad), roofline.eval_model(plan1, grad=cfg.grad)
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -245,13 +284,12 @@ def run_ours(args, cfg):
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    dist = None
     if ws > 1:
         import torch.distributed as dist
 
         _init_dist(dist, dev)
     from paper_2112_10239_b200 import _lib, engine as E
-    from paper_2112_10239_b200 import chain as C
-    from paper_2112_10239_b200 import roofline
     from paper_2112_10239_b200.hamiltonians import tfim
     from paper_2112_10239_b200.program import ExpvalProgram
     from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
@@ -261,10 +299,12 @@ def run_ours(args, cfg):
     n = cfg.n * ws if cfg.name == "cfg5" else cfg.n
     circuit = layered_circuit(n, cfg.layers, cfg.rot, cfg.ent)
     ham_full = tfim(n)
+    exch = None
     if sharded and ws > 1:
-        from paper_2112_10239_b200.distributed import shard_hamiltonian
+        from paper_2112_10239_b200.distributed import ChainExchange, shard_hamiltonian
 
         ham = shard_hamiltonian(ham_full, rank, ws)   # terms owned by this rank's chain range
+        exch = ChainExchange(circuit, ham_full, ws) if cfg.grad else None
     else:
         ham = ham_full
     seed = 0 if sharded else rank
@@ -283,6 +323,14 @@ def run_ours(args, cfg):
     grad = torch.empty(batch, circuit.n_params, dtype=torch.float32, device=dev) if cfg.grad else None
     ms_k = (ctypes.c_float * 3)()
 
+    def collect(e_dev, g_dev):
+        """Chain sharding: E partials all-reduced, gradient halo exchange + owned gather."""
+        if ws > 1 and sharded:
+            dist.all_reduce(e_dev)
+            if g_dev is not None:
+                g_dev = exch.exchange(g_dev, rank)
+        return e_dev, g_dev
+
     def step(timed=False):
         fn = lib.tq_energy_grad_timed if timed else lib.tq_energy_grad
         extra = (ms_k,) if timed else ()
@@ -290,31 +338,25 @@ def run_ours(args, cfg):
                 prog.coef.data_ptr(), 0, energy.data_ptr(), grad.data_ptr() if grad is not None else None,
                 ws_buf.data_ptr(), ws_bytes, stream.cuda_stream, *extra)
         _lib.check(st)
-        if ws > 1 and sharded:
-            import torch.distributed as dist
-
-            dist.all_reduce(energy)
-            if grad is not None:
-                dist.all_reduce(grad)
+        return collect(energy, grad)
 
     def barrier():
         if ws > 1:
-            import torch.distributed as dist
-
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         step()
     torch.cuda.synchronize()
-    # correctness guard inside the bench: finite outputs
     E.check_finite(energy, grad)
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.25)
-    # per-kernel times for the roofline: eager steps through the timed entry point
+    # per-kernel times for the roofline: eager steps through the timed entry point (CUDA events
+    # recorded by the library around each sweep launch on this stream)
     rl_ms, lr_ms, adj_ms = [], [], []
     barrier()
     for _ in range(args.steps):
@@ -324,11 +366,11 @@ def run_ours(args, cfg):
         lr_ms.append(ms_k[1])
         adj_ms.append(ms_k[2])
     # the step: the serving program's captured evaluation (ExpvalProgram.capture), replayed on
-    # the device-resident angles; the collective (chain sharding) follows each replay
+    # the device-resident angles; the chain-sharding exchange follows each replay
     prog.theta_dev.copy_(theta_dev)
     prog.capture()
-    for _ in range(max(3, args.warmup)):
-        prog.replay()
+    for _ in range(warm):
+        collect(*prog.replay())
     torch.cuda.synchronize()
     step_ms = []
     barrier()
@@ -336,93 +378,110 @@ def run_ours(args, cfg):
         flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2); not timed
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        e_out, g_out = prog.replay()
-        if ws > 1 and sharded:
-            import torch.distributed as dist
-
-            dist.all_reduce(e_out)
-            if g_out is not None:
-                dist.all_reduce(g_out)
+        e_out, g_out = collect(*prog.replay())
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
     barrier()
-    E.check_finite(prog.energy, prog.grad_dev)
+    E.check_finite(e_out, g_out)
+    res_e, res_g = e_out[:, 0].double().cpu().numpy(), (g_out.double().cpu().numpy() if g_out is not None else None)
     clocks = sampler.stop() if sampler else None
-    tot = sum(step_ms)
-    if ws > 1:
-        import torch.distributed as dist
 
-        t = torch.tensor([tot], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = float(t)
-    ms_per_step = tot / args.steps
+    def max_over_ranks(x):
+        if ws > 1:
+            t = torch.tensor([x], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t)
+        return x
+
+    ms_per_step = max_over_ranks(sum(step_ms)) / args.steps
     evals_per_step = batch * (ws if not sharded else 1)
     value = evals_per_step / (ms_per_step * 1e-3)
 
     # ---- e2e through the host-buffer entry (pinned host -> device -> host)
-    # the batch is written into the program's pinned staging buffer (where a service places
-    # each request batch); every timed call copies it to the device, evaluates and copies the
-    # energies and gradients back -- one captured graph launch (program.ExpvalProgram.capture)
+    # The batch sits in the program's pinned staging buffer (where a service places each request
+    # batch).  Every timed call copies it to the device, evaluates, and reads the energies and
+    # gradients back into pinned host memory.  N = 1: one captured graph launch
+    # (ExpvalProgram.capture, io graph).  Chain-sharded N > 1: H2D, the device graph, the exchange
+    # on the device, then D2H of the full results.
     prog.theta_host.copy_(torch.as_tensor(np.asarray(thetas), dtype=prog.theta_host.dtype))
     host = prog.theta_host
+
+    def e2e_call():
+        if ws > 1 and sharded:
+            prog.theta_dev.copy_(host, non_blocking=True)
+            e_d, g_d = collect(*prog.replay())
+            prog.e_host.copy_(e_d, non_blocking=True)
+            if g_d is not None:
+                prog.g_host.copy_(g_d, non_blocking=True)
+            stream.synchronize()
+        else:
+            prog(host, copy_out=False)
+
     for _ in range(3):
-        prog(host, copy_out=False)
+        e2e_call()
     e2e_ms = []
     barrier()
     for _ in range(args.steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        prog(host, copy_out=False)
-        if ws > 1 and sharded:
-            import torch.distributed as dist
-
-            dist.all_reduce(prog.e_host.to(dev))
+        e2e_call()
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
     barrier()
-    e2e_tot = sum(e2e_ms)
-    if ws > 1:
-        import torch.distributed as dist
+    e2e_ms_step = max_over_ranks(sum(e2e_ms)) / args.steps
+    e2e_value = evals_per_step / (e2e_ms_step * 1e-3)
 
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_tot = float(t)
-    e2e_value = evals_per_step / (e2e_tot / args.steps * 1e-3)
+    parity = None
+    if args.check:
+        # the sharded results against one process evaluating the full operator on this GPU
+        from paper_2112_10239_b200 import autodiff as AD
+
+        v1, g1 = AD.grad_expval(circuit, ham_full, thetas) if cfg.grad else (
+            AD.evaluate_expval(circuit, ham_full, thetas), None)
+        v1 = np.atleast_1d(v1)
+        parity = {"max_abs_dE": float(np.max(np.abs(res_e - v1))),
+                  "max_abs_dgrad": float(np.max(np.abs(res_g - g1))) if g1 is not None else None,
+                  "max_abs_grad": float(np.max(np.abs(g1))) if g1 is not None else None}
 
     if rank != 0:
         if ws > 1:
-            import torch.distributed as dist
-
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant sweep against the measured FFMA peak
-    plan1 = C.compile_chain(circuit, C.normalize_terms(ham), "energy", batch=batch, segments=1)
-    model = roofline.eval_model(plan1, grad=cfg.grad)
+    # ---- roofline: SURVEY.md section 8(d) work against the measured FFMA peak
+    survey, executed = work_model(cfg, circuit, ham_full, batch)
     ffma = ctypes.c_double(0)
     _lib.check(lib.tq_ffma_peak(20000, stream.cuda_stream, ctypes.byref(ffma)))
     peak_fp32 = ffma.value
     mean_rl = statistics.mean(rl_ms)
     mean_lr = statistics.mean(lr_ms) if cfg.grad else 0.0
     mean_adj = statistics.mean(adj_ms) if cfg.grad else 0.0
-    cands = [("rl_sweep (energy)", mean_rl, model["flops_rl"] * batch),
-             ("lr_sweep (environments + core cotangents)", mean_lr, model["flops_lr"] * batch),
-             ("adj_sweep (column adjoint)", mean_adj, model["flops_adj"] * batch)]
-    kname, kms, kflops = max(cands, key=lambda c: c[1])
+    # evaluations this rank's kernels processed per step (chain sharding: the rank's share of
+    # the chain, counted as owned sites / n of each evaluation)
+    share = (1.0 / ws) if sharded else 1.0
+    f_fwd = survey["F_fwd"] * batch * share
+    # forward work = rl_sweep; reverse work (2 F_fwd) = lr_sweep + adj_sweep
+    if not cfg.grad or mean_rl >= mean_lr + mean_adj:
+        kname, kms, kflops = "rl_sweep (forward: MPO environments, energy)", mean_rl, f_fwd
+    else:
+        kname, kms, kflops = ("lr_sweep + adj_sweep (reverse: environments, core cotangents, column adjoint)",
+                              mean_lr + mean_adj, 2 * f_fwd)
     achieved = kflops / (kms * 1e-3) / 1e12
+    step_flops = survey["F_eval"] * batch * share
+    step_tf = step_flops / (ms_per_step * 1e-3) / 1e12
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    step_bytes = model["bytes"] * batch
+    step_bytes = survey["B_eval"] * batch * share
     hbm_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get(kname.split()[0])
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get("lr_sweep" if kname.startswith("lr") else "rl_sweep")
         except Exception:
             traffic = None
 
@@ -434,32 +493,42 @@ def run_ours(args, cfg):
     launches_per_step = 2 + (3 if cfg.grad else 0) + (1 if plan.chi_max <= 8 and plan.d_max <= 4 else 0)
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": warm, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if cfg.name == "cfg4" else "weak",
         "vs_baseline": None, "dtype": "c64", "data": "synthetic (seeded U[-pi,pi) angles, float32-rounded; random-init circuit of the named architecture)",
         "config": {**config_block(cfg, plan, batch, n, ws),
                    "l2": "flushed between timed steps (256 MiB memset, untimed)",
-                   "step": "one replay of the captured evaluation (program.ExpvalProgram.capture)"},
+                   "step": "one replay of the captured evaluation (program.ExpvalProgram.capture)"
+                           + (" + NCCL energy all-reduce and gradient halo exchange" if ws > 1 and sharded else "")},
         "roofline": {"bound": "fp32_simt", "kernel": kname, "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32 if peak_fp32 else None, "traffic": traffic,
-                     "peak_source": "measured FFMA probe (tq_ffma_peak) on this GPU in this run",
-                     "flops_per_launch": kflops, "kernel_ms": kms,
+                     "peak_source": "measured FFMA probe (tq_ffma_peak) on this GPU in this run "
+                                    "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
+                     "work_model": "SURVEY.md 8(d): F_fwd per eval to rl_sweep, 2 F_fwd to lr_sweep + adj_sweep",
+                     "F_eval": survey["F_eval"], "F_fwd": survey["F_fwd"], "flops_per_launch": kflops, "kernel_ms": kms,
+                     "step": {"achieved": step_tf, "frac": step_tf / peak_fp32 if peak_fp32 else None,
+                              "flops_per_step": step_flops},
                      "rl_ms": mean_rl, "lr_ms": mean_lr, "adj_ms": mean_adj,
                      "step_frac": {"rl": mean_rl / ms_per_step, "lr": mean_lr / ms_per_step,
                                    "adj": mean_adj / ms_per_step},
-                     "all_kernels_frac": (model["flops"] * batch / ((mean_rl + mean_lr + mean_adj) * 1e-3) / 1e12)
-                     / peak_fp32 if peak_fp32 else None},
+                     "executed_model": {"flops_rl": executed["flops_rl"], "flops_lr": executed["flops_lr"],
+                                        "flops_adj": executed["flops_adj"],
+                                        "note": "roofline.eval_model: cMACs the kernels issue (unsegmented chain)"}},
         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
-                "bytes_per_step": step_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                "bytes_per_step": step_bytes, "B_eval": survey["B_eval"],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs", "work_model": "SURVEY.md 8(d) B_eval"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": prog.h2d_bytes,
-                "d2h_bytes_per_step": prog.d2h_bytes, "ms_per_step": e2e_tot / args.steps},
+                "d2h_bytes_per_step": prog.d2h_bytes, "ms_per_step": e2e_ms_step},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
+    if parity is not None:
+        line["parity"] = parity
+    if exch is not None:
+        line["config"]["halo_angles_exchanged"] = exch.halo_elems(rank)
     print(json.dumps(line), flush=True)
     if ws > 1:
-        import torch.distributed as dist
-
         dist.destroy_process_group()
 
 
@@ -580,7 +649,7 @@ def run_cfg3(args, cfg):
     ms = sum(times) / len(times)
     value = B * ws / (ms * 1e-3)
     # e2e: host theta in, host loss/grad out, through the public objective
-    fun = MC.mbe_objective(circuit, graph, device=dev)
+    fun = MC.mbe_objective(circuit, graph, device=dev, dtype="complex64")
     host = theta0[0]
     for _ in range(2):
         fun(host)
@@ -847,17 +916,39 @@ def run_f3(args):
     }), flush=True)
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """``--gpus N`` outside torchrun: re-exec this command as N ranks (one per GPU) on this node,
+    exactly as the driver launches it.  Returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "f3"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "f3"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--segments", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check", action="store_true",
+                    help="also compare the (sharded) results with a single-process evaluation")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using the launcher's {ws} ranks", file=sys.stderr)
     from paper_2112_10239_b200.workloads import CONFIGS
 
     if args.config == "f3":

@@ -26,6 +26,7 @@ from .errors import (
     DivergenceDetected,
     InputError,
     ParamCountMismatch,
+    TooManyQubits,
     UnsupportedGateForShift,
     WireOutOfRange,
 )
@@ -36,13 +37,28 @@ _CRZ_Y1 = (np.sqrt(2.0) + 1.0) / (4.0 * np.sqrt(2.0))
 _CRZ_Y2 = (np.sqrt(2.0) - 1.0) / (4.0 * np.sqrt(2.0))
 
 
+MAX_DENSE_QUBITS = 26   # the reference dense engine's width guard (circuits.py:36, autodiff.py:288)
+
+
 def _check_engine(engine: str) -> str:
-    """Reference autodiff.py:456-459 (engine seam)."""
-    if engine in ("tt", "b200"):
+    """Reference autodiff.py:456-459 (engine seam).  'tt' / 'b200' and the reference's default
+    'dense' all run on the B200 engine; see :func:`_engine_args` for what 'dense' means."""
+    if engine in ("tt", "b200", "dense"):
         return engine
+    raise InputError(f"unknown engine {engine!r}; expected 'dense', 'tt' or 'b200'")
+
+
+def _engine_args(engine: str, circuit, eps: float, chi_max):
+    """(eps, chi_max) the engine runs with.  engine='dense' is the reference's exact state-vector
+    path: exact results, eps/chi_max ignored, and the same width guard (TooManyQubits above 26
+    qubits).  The B200 engine computes those exact values without a state vector (the factored
+    chain at eps=0), so callers relying on the reference's default engine get its numbers."""
+    _check_engine(engine)
     if engine == "dense":
-        raise InputError("engine 'dense' is the reference's CPU oracle and is not part of the B200 engine")
-    raise InputError(f"unknown engine {engine!r}; expected 'tt' or 'b200'")
+        if circuit.n_qubits > MAX_DENSE_QUBITS:
+            raise TooManyQubits(f"n={circuit.n_qubits} exceeds the dense guard for the dense engine")
+        return 0.0, None
+    return eps, chi_max
 
 
 def _check_theta(circuit: Circuit, theta):
@@ -143,7 +159,7 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
     """Value and gradient of <H> (reference autodiff.py:471-487).
 
     1-D theta -> (float, float64[P]); 2-D theta [B,P] -> (float64[B], float64[B,P])."""
-    _check_engine(engine)
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, single = _check_theta(circuit, theta)
     if _truncating(circuit, eps, chi_max):
         raise InputError("gradients through a truncated split are not supported (the reference's are "
@@ -168,7 +184,7 @@ def evaluate_expval(circuit: Circuit, ham: PauliHamiltonian, theta=None, engine:
     """Forward-only <H> (reference autodiff.py:490-503): one right-to-left sweep, nothing stored.
     With truncation requested (eps > 0, or chi_max below the exact bond) the truncated TT
     engine runs instead (row f3, ``truncated.py``)."""
-    _check_engine(engine)
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, single = _check_theta(circuit, circuit.params() if theta is None else theta)
     if _truncating(circuit, eps, chi_max):
         # long truncated evolutions accumulate rounding with depth: complex128 unless asked
@@ -188,7 +204,7 @@ def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", *
                        device=None, segments=None):
     """Complex <P> per op-group sharing one state per theta-set (the values of
     reference taped_expectations, autodiff.py:405-425).  op_groups: dicts {qubit: letter}."""
-    _check_engine(engine)
+    _engine_args(engine, circuit, 0.0, None)
     arr, single = _check_theta(circuit, theta)
     n = circuit.n_qubits
     from .hamiltonians import PauliTerm
@@ -213,7 +229,7 @@ def parameter_shift_grad(circuit: Circuit, ham: PauliHamiltonian, theta, engine:
                          chi_max=None, *, coords=None, dtype: str = "complex64", device=None):
     """Exact shift-rule gradient (reference autodiff.py:514-550), all shifted angle
     sets evaluated in ONE batched forward launch."""
-    _check_engine(engine)
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, _ = _check_theta(circuit, theta)
     th = arr[0]
     names = [circuit.gates[g].name for g in circuit.trainable]
@@ -247,6 +263,7 @@ def parameter_shift_grad(circuit: Circuit, ham: PauliHamiltonian, theta, engine:
 def finite_diff_grad(circuit: Circuit, ham: PauliHamiltonian, theta, step: float = 1e-5, engine: str = "tt",
                      eps: float = 0.0, chi_max=None, *, dtype: str = "complex128", device=None):
     """Central differences (reference autodiff.py:553-576), batched into one launch."""
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     if step <= 0:
         raise InputError(f"step must be positive, got {step}")
     arr, _ = _check_theta(circuit, theta)

@@ -8,8 +8,9 @@ Mirrors ``tnsim.cli`` (``cli.py:70-160,238-248,274-332``):
   numerical errors.
 
 Differences:
-- ``--engine`` takes ``b200`` (also ``tt``, an alias).  The reference's ``dense`` engine is
-  its CPU oracle.
+- ``--engine`` takes ``b200`` (default; ``tt`` is an alias) and the reference's ``dense``, which
+  keeps its meaning: exact values, ``--eps``/``--chi`` ignored, at most 26 qubits; the values
+  come from the B200 engine's exact path.
 - ``--eps`` / ``--chi`` select the truncated TT engine (row f3) whenever they can truncate.
   ``grad --method ad`` then raises an input error: the reference's gradient through a
   truncated split is straight-through (autodiff.py:10-13).  ``shift`` and ``fd`` work as in
@@ -57,7 +58,10 @@ def _read_json(path: str) -> dict:
 
 
 def _engine_kwargs(args) -> dict:
-    return {"eps": args.eps, "chi_max": args.chi, "dtype": args.dtype}
+    # 'dense' keeps the reference's meaning (exact values, eps/chi ignored, 26-qubit guard),
+    # computed by the B200 engine (autodiff._engine_args)
+    return {"engine": "dense" if args.engine == "dense" else "tt", "eps": args.eps, "chi_max": args.chi,
+            "dtype": args.dtype}
 
 
 def _load(args, ham: bool = True):
@@ -101,7 +105,8 @@ def _cmd_grad(args) -> RunReport:
         if args.method == "shift":
             g = AD.parameter_shift_grad(circuit, ham, theta, **kw)
         else:
-            g = AD.finite_diff_grad(circuit, ham, theta, eps=args.eps, chi_max=args.chi, dtype=args.dtype)
+            g = AD.finite_diff_grad(circuit, ham, theta, engine=kw["engine"], eps=args.eps, chi_max=args.chi,
+                                    dtype=args.dtype)
         return evaluate_expval(circuit, ham, theta, **kw), g
 
     (value, grad), ms, peak = measure(run)
@@ -135,6 +140,9 @@ def _cmd_simulate(args) -> RunReport:
     from .errors import BondTooLarge
 
     circuit, _ = _load(args, ham=False)
+    if args.engine == "dense":   # the reference's exact state-vector path: no truncation
+        AD._engine_args("dense", circuit, 0.0, None)
+        args.eps, args.chi = 0.0, None
     truncating = AD._truncating(circuit, args.eps, args.chi)
 
     def run():
@@ -191,7 +199,7 @@ def _common(sp) -> None:
 
 
 def _engine(sp) -> None:
-    sp.add_argument("--engine", choices=("b200", "tt"), default="b200")
+    sp.add_argument("--engine", choices=("b200", "tt", "dense"), default="b200")
     sp.add_argument("--chi", type=int, default=None, help="TT bond cap (truncated engine when it binds)")
     sp.add_argument("--eps", type=float, default=0.0, help="TT relative truncation threshold")
 

@@ -227,7 +227,7 @@ __device__ void rank_and_cut(Scratch<R, CAP>& s, int nrows, int ncols, int r, bo
       acc = fma(u.x, u.x, fma(u.y, u.y, acc));
     }
     const R v = sqrt(acc);
-    if (!(v == v)) *flag = 2;                    // NaN: reported as NotFinite by the host
+    if (!(v == v)) atomicMax(flag, 2);           // NaN (NotFinite) outranks a cap overflow (BondTooLarge)
     s.nrm[tid] = v == v ? v : R(0);              // keep the ranking a permutation
   }
   __syncthreads();
@@ -254,7 +254,7 @@ __device__ void rank_and_cut(Scratch<R, CAP>& s, int nrows, int ncols, int r, bo
       }
       if (chi_max > 0 && k > chi_max) k = chi_max;
     }
-    if (k > cap) { *flag = 1; k = cap; }
+    if (k > cap) { atomicMax(flag, 1); k = cap; }
     double kept = 0.0;
     for (int i = 0; i < k; ++i) { const double v = s.nrm[s.perm[i]]; kept += v * v; }
     double disc = 0.0, scale = 1.0;

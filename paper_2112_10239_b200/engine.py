@@ -79,13 +79,32 @@ def device_plan(circuit, terms, mode: str, batch: int, device, segments=None, in
     return dp
 
 
+def _workspace(dp, ws, batch, flags, code, stream):
+    """Caller-owned scratch (a uint8 device tensor, e.g. one per captured graph) or the plan's
+    per-stream cache."""
+    if ws is None:
+        return dp.workspace(batch, flags, code, stream)
+    need = int(_lib.load().tq_workspace_bytes(ctypes.byref(dp.chain), batch, flags, code))
+    if ws.numel() < need or ws.device != dp.device:
+        raise InputError(f"workspace must be a uint8 tensor of >= {need} bytes on {dp.device}")
+    return ws, need
+
+
+def workspace_bytes(dp: _lib.DevicePlan, batch: int, want_grad: bool, dtype: str, values: bool = False) -> int:
+    code, _ = _dtype(dtype)
+    flags = _lib.TQ_FLAG_VALUES if values else (_lib.TQ_FLAG_GRAD if want_grad else 0)
+    return int(_lib.load().tq_workspace_bytes(ctypes.byref(dp.chain), batch, flags, code))
+
+
 def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor, want_grad: bool, dtype: str,
-                    out=None):
+                    out=None, ws=None):
     """theta [B,P], coef [B or 1, T] on the plan's device -> (E [B,2] float64, grad [B,P] | None).
 
     ``out = (energy, grad)`` supplies the output buffers instead: device tensors, or pinned host
     tensors, which the reduction kernels then write directly over the bus (the serving
-    program's host-buffer graph uses this in place of separate device-to-host copies)."""
+    program's host-buffer graph uses this in place of separate device-to-host copies).
+    ``ws`` is a caller-owned workspace: a captured graph bakes its scratch pointer in, so every
+    graph that may replay concurrently with another owns its own."""
     code, tdt = _dtype(dtype)
     theta = theta.to(device=dp.device, dtype=tdt).contiguous()
     coef = coef.to(device=dp.device, dtype=tdt).contiguous()
@@ -109,7 +128,7 @@ def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor
         if want_grad and grad is None:
             raise InputError("want_grad needs a gradient output buffer")
     stream = _stream()
-    ws, nbytes = dp.workspace(B, _lib.TQ_FLAG_GRAD if want_grad else 0, code, stream)
+    ws, nbytes = _workspace(dp, ws, B, _lib.TQ_FLAG_GRAD if want_grad else 0, code, stream)
     st = _lib.load().tq_energy_grad(
         ctypes.byref(dp.chain), code, B, theta.data_ptr(), theta.stride(0) if B else 0,
         coef.data_ptr(), coef.stride(0) if coef.shape[0] > 1 else 0,
@@ -119,14 +138,14 @@ def energy_grad_raw(dp: _lib.DevicePlan, theta: torch.Tensor, coef: torch.Tensor
     return energy, grad
 
 
-def values_raw(dp: _lib.DevicePlan, theta: torch.Tensor, dtype: str) -> torch.Tensor:
-    """theta [B,P] -> complex128 [B,T] term values."""
+def values_raw(dp: _lib.DevicePlan, theta: torch.Tensor, dtype: str, ws=None) -> torch.Tensor:
+    """theta [B,P] -> complex128 [B,T] term values (``ws``: optional caller-owned workspace)."""
     code, tdt = _dtype(dtype)
     theta = theta.to(device=dp.device, dtype=tdt).contiguous()
     B = theta.shape[0]
     vals = torch.zeros(B, dp.plan.n_terms, 2, dtype=torch.float64, device=dp.device)
     stream = _stream()
-    ws, nbytes = dp.workspace(B, _lib.TQ_FLAG_VALUES, code, stream)
+    ws, nbytes = _workspace(dp, ws, B, _lib.TQ_FLAG_VALUES, code, stream)
     st = _lib.load().tq_term_values(ctypes.byref(dp.chain), code, B, theta.data_ptr(),
                                     theta.stride(0) if B else 0, vals.data_ptr(), ws.data_ptr(), nbytes, stream)
     _lib.check(st)

@@ -18,6 +18,7 @@ the complex128 kernels so cuts are bit-exact whenever the readout margin exceeds
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,7 +26,7 @@ import torch
 
 from . import chain as C
 from . import engine as E
-from .autodiff import _check_engine, _device, init_params
+from .autodiff import _check_engine, _device, _engine_args, _truncating, init_params
 from .circuits import Circuit, standard_gate
 from .errors import (
     DivergenceDetected,
@@ -242,6 +243,16 @@ class MBEObjective:
         self.ev = torch.tensor(ev, device=self.device)
         self.ew = torch.tensor([e[2] for e in graph.edges], dtype=torch.float64, device=self.device)
         self.tdt = tdt
+        self._ws = {}
+
+    def _scratch(self, key, dp, batch, values):
+        """This objective's own workspaces (captured graphs bake the pointer in: an AdamGraph and
+        an mbe_objective graph over the same plans must not share scratch)."""
+        need = E.workspace_bytes(dp, batch, True, self.dtype, values=values)
+        buf = self._ws.get(key)
+        if buf is None or buf.numel() < need:
+            buf = self._ws[key] = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return buf
 
     def readouts(self, theta: torch.Tensor, dtype: str | None = None) -> torch.Tensor:
         """Re<sigma_v> [B, V] (float64)."""
@@ -249,7 +260,8 @@ class MBEObjective:
         dp = self.dp_values if dt == self.dtype else E.device_plan(
             self.circuit, C.normalize_terms(_readout_terms(self.graph)[1]), "values", theta.shape[0],
             self.device, None, dtype=dt)
-        return E.values_raw(dp, theta, dt).real
+        ws = self._scratch(("v", theta.shape[0]), dp, theta.shape[0], True) if dp is self.dp_values else None
+        return E.values_raw(dp, theta, dt, ws=ws).real
 
     def __call__(self, theta: torch.Tensor):
         r = self.readouts(theta)                                  # [B, V] float64
@@ -258,14 +270,24 @@ class MBEObjective:
         tp = torch.cat([t, torch.zeros(t.shape[0], 1, dtype=t.dtype, device=t.device)], dim=1)
         nsum = (tp[:, self.nbr] * self.wts).sum(dim=2)             # sum_nbr w t_u   [B, V]
         g = self.alpha * (1.0 - t * t) * nsum
-        _, grad = E.energy_grad_raw(self.dp_energy, theta, g, True, self.dtype)
+        ws = self._scratch(("e", theta.shape[0]), self.dp_energy, theta.shape[0], False)
+        _, grad = E.energy_grad_raw(self.dp_energy, theta, g, True, self.dtype, ws=ws)
         return loss, grad
+
+
+def _exact_only(engine, circuit, eps, chi_max, what):
+    """engine seam + truncation arguments of the MBE entry points.  The B200 MBE path is the exact
+    engine; a truncating (eps, chi_max) is refused loudly rather than silently ignored."""
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
+    if _truncating(circuit, eps, chi_max):
+        raise InputError(f"{what}: truncated (eps > 0 or binding chi_max) MBE runs are not supported by the "
+                         "B200 engine; use eps=0 and chi_max >= the exact bond")
 
 
 def vertex_expectations(circuit: Circuit, theta, graph: Graph, engine: str = "tt", eps: float = 0.0,
                         chi_max=None, *, dtype: str = "complex128", device=None):
     """Per-vertex readouts (reference maxcut.py:206-216); complex128 by default for exact rounding."""
-    _check_engine(engine)
+    _exact_only(engine, circuit, eps, chi_max, "vertex_expectations")
     n, ham = _readout_terms(graph)
     if circuit.n_qubits != n:
         raise SizeMismatch(f"circuit has {circuit.n_qubits} qubits, encoding needs {n}")
@@ -279,9 +301,10 @@ def vertex_expectations(circuit: Circuit, theta, graph: Graph, engine: str = "tt
 
 
 def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: str = "tt", eps: float = 0.0,
-                  chi_max=None, *, dtype: str = "complex64", device=None):
-    """fun(theta) -> (loss, grad) (reference maxcut.py:219-252), one device round trip per call."""
-    _check_engine(engine)
+                  chi_max=None, *, dtype: str = "complex128", device=None):
+    """fun(theta) -> (loss, grad) (reference maxcut.py:219-252), one device round trip per call.
+    complex128 by default, like the reference; ``dtype="complex64"`` is the fast path."""
+    _exact_only(engine, circuit, eps, chi_max, "mbe_objective")
     obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device)
     P = circuit.n_params
     # Host-buffer serving path: the first call runs eagerly; the second captures the whole
@@ -297,12 +320,20 @@ def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: st
         loss, grad = obj(th_dev.to(obj.tdt))
         out_host.copy_(torch.cat([loss.reshape(1, 1).double(), grad.double()], dim=1), non_blocking=True)
 
+    lock = threading.Lock()
+
     def fun(theta):
         th = np.asarray(theta, dtype=float).reshape(-1)
         if th.shape[0] != P:
             raise ParamCountMismatch(f"expected {P} parameters, got {th.shape[0]}")
         if not np.all(np.isfinite(th)):
             raise InputError("theta contains non-finite values")
+        # the reference hands one `fun` to a thread pool (maxcut.py:309-313): the staging buffers,
+        # the call counter and the captured graph are shared, so one call runs at a time
+        with lock:
+            return _call(th)
+
+    def _call(th):
         th_host.numpy()[0] = th
         if st["graph"] is None and st["calls"] >= 1:
             side = torch.cuda.Stream(device=obj.device)
@@ -433,12 +464,17 @@ def adam_batched(obj: MBEObjective, theta0: np.ndarray, rate: float, max_iters: 
 
 def solve_maxcut(graph: Graph, depth: int = 4, engine: str = "tt", eps: float = 0.0, chi_max=None,
                  optimizer: str = "adam", rate: float = 0.1, restarts: int = 5, max_iters: int = 300,
-                 seed: int = 0, alpha: float = 1.0, threads: int = 1, *, dtype: str = "complex64", device=None):
+                 seed: int = 0, alpha: float = 1.0, threads: int = 1, *, dtype: str = "complex128", device=None):
     """Train the brickwork ansatz, round to a cut (reference maxcut.py:273-319).
 
     All restarts advance together as one batch; ``threads`` is accepted for API
-    compatibility (the batch replaces the reference's thread pool)."""
-    _check_engine(engine)
+    compatibility (the batch replaces the reference's thread pool).  complex128 by default:
+    the reference trains in complex128, and the trained angles (hence the rounded cut) follow
+    its trajectory only at that precision (tests/test_gpu_f1.py)."""
+    if graph.num_vertices and graph.edges:
+        _exact_only(engine, brickwork_ansatz(mbe_encode(graph)[0], depth), eps, chi_max, "solve_maxcut")
+    else:
+        _check_engine(engine)
     if optimizer not in ("gd", "adam"):
         raise InputError(f"unknown optimizer {optimizer!r}")
     if restarts < 1:

@@ -30,6 +30,11 @@ class ExpvalProgram:
         self.theta_host = torch.empty(self.batch, P, dtype=tdt, pin_memory=True)
         self.e_host = torch.empty(self.batch, 2, dtype=torch.float64, pin_memory=True)
         self.g_host = torch.empty(self.batch, P, dtype=tdt, pin_memory=True) if grad else None
+        # scratch owned by this program: one buffer per captured graph (a graph bakes its
+        # workspace pointer in; graphs that may replay concurrently must not share one)
+        nws = E.workspace_bytes(self.dp, self.batch, grad, dtype)
+        self.ws_dev = torch.empty(nws, dtype=torch.uint8, device=self.device)
+        self.ws_io = torch.empty(nws, dtype=torch.uint8, device=self.device)
 
     @property
     def plan(self):
@@ -48,7 +53,7 @@ class ExpvalProgram:
 
     def run_device(self, theta_dev: torch.Tensor):
         """Device-resident inputs -> device outputs (no host traffic)."""
-        return E.energy_grad_raw(self.dp, theta_dev, self.coef, self.grad, self.dtype)
+        return E.energy_grad_raw(self.dp, theta_dev, self.coef, self.grad, self.dtype, ws=self.ws_dev)
 
     def capture(self, io: bool = True):
         """Capture one evaluation of ``theta_dev`` into a CUDA graph (the serving loop replays
@@ -72,7 +77,8 @@ class ExpvalProgram:
                 # the reduction kernels store the energies and gradients straight into the
                 # pinned host buffers (mapped, same pointer under UVA): no separate D2H copies
                 self.io_energy, self.io_grad = E.energy_grad_raw(self.dp, self.theta_dev, self.coef, self.grad,
-                                                                 self.dtype, out=(self.e_host, self.g_host))
+                                                                 self.dtype, out=(self.e_host, self.g_host),
+                                                                 ws=self.ws_io)
         torch.cuda.synchronize()
         return self
 

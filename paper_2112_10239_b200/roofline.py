@@ -69,3 +69,28 @@ def eval_model(plan, grad: bool = True, real_bytes: int = 4) -> dict:
         byts += P * real_bytes + 2 * env_bytes(plan, real_bytes)
     return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops_adj": flops_adj,
             "flops": flops_rl + flops_lr + flops_adj, "bytes": byts, "cmacs": c}
+
+
+def survey_model(plan, n_terms_1: int, n_terms_2: int, layers: int, grad: bool = True) -> dict:
+    """SURVEY.md section 8(d)'s official per-evaluation work (the judge's formulas).
+
+    ``plan`` must be the UNSEGMENTED plan (segments=1) so its sites carry the bonds
+    chi_k = 2^{c_k} of the factored chain (chi_0 = chi_n = 1).  Per site k:
+      step_k = 2 chi_k chi_{k+1} (chi_k + chi_{k+1}) cMAC   (one transfer sum_s A_s^H E A_s)
+      fold_k = 4 L chi_k chi_{k+1} cMAC                     (L = rows + lines)
+      F_fwd  = 8 [sum fold + 2 sum step + (T1 + 2 T2) mean(step)]   real flops
+      F_eval = 3 F_fwd with the gradient, F_fwd forward-only
+      B_eval = 4P + 4P + 4 + 16 sum_k chi_k^2 bytes (gradient), 4P + 4 forward-only."""
+    s = plan.sites
+    cl = s["chi_l"].astype(np.float64)
+    cr = s["chi_r"].astype(np.float64)
+    step = 2 * cl * cr * (cl + cr)
+    fold = 4 * layers * cl * cr
+    f_fwd = 8 * (fold.sum() + 2 * step.sum() + (n_terms_1 + 2 * n_terms_2) * step.mean())
+    P = plan.n_params
+    if grad:
+        chi2 = float(np.sum(cr[:-1] ** 2)) if len(cr) > 1 else 0.0   # cuts 1..n-1
+        byts = 4 * P + 4 * P + 4 + 16 * chi2
+    else:
+        byts = 4 * P + 4
+    return {"F_fwd": float(f_fwd), "F_eval": float(3 * f_fwd if grad else f_fwd), "B_eval": float(byts)}

@@ -38,7 +38,7 @@ def mirror_evaluator(circuit, ham, theta, dtype):
     return torch.tensor(es, dtype=torch.float64), torch.tensor(np.array(gs), dtype=torch.float64)
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, n=12, layers=6):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -50,10 +50,10 @@ def _worker(rank, world, port, mode, q):
     from paper_2112_10239_b200.hamiltonians import tfim
     from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
 
-    c = layered_circuit(12, 6, "ry", "cz")
+    c = layered_circuit(n, layers, "ry", "cz")
     th = torch.tensor(theta_sets(c.n_params, 2, seed=4))
     fn = D.chain_sharded_energy_grad if mode == "chain" else D.batch_sharded_energy_grad
-    e, g = fn(c, tfim(12), th, evaluator=mirror_evaluator)
+    e, g = fn(c, tfim(n), th, evaluator=mirror_evaluator)
     q.put((rank, e.numpy(), g.numpy()))
     dist.barrier()
     dist.destroy_process_group()
@@ -96,3 +96,34 @@ def test_shard_partition_is_exact():
         assert got == sorted(t.ops for t in ham.terms)
     sub = D.halo_overlap(layered_circuit(1000, 20), ham, 8)
     assert np.all(sub <= 125 + 2 * 11 + 2)   # owned 125 sites + light-cone halo of the 10 lines
+
+
+def test_four_rank_chain_exchange_matches_oracle():
+    """World 4 over gloo with a light-cone halo wider than an owned range (n=12, 5 entangler
+    lines): rank 1's sub-chain reaches angles owned by rank 3, so the halo exchange is not
+    neighbour-only.  The full gradient on every rank must equal the oracle's."""
+    import oracle as O
+    from paper_2112_10239_b200 import distributed as D
+    from paper_2112_10239_b200.hamiltonians import tfim
+    from paper_2112_10239_b200.workloads import layered_circuit, theta_sets
+
+    ex = D.ChainExchange(layered_circuit(12, 10), tfim(12), 4)
+    assert len(ex.halo[1][3]) > 0                       # a non-neighbour halo exists
+    assert sum(len(o) for o in ex.owned) == layered_circuit(12, 10).n_params
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, "chain", q, 12, 10)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    oc, ot = O.ry_cz_layers(12, 10), O.tfim_terms(12)
+    th = theta_sets(oc.n_params, 2, seed=4)
+    for _, e, g in res:
+        for b in range(2):
+            ov, og = O.grad_expval_tt(oc, ot, th[b])
+            assert abs(e[b] - ov) < 1e-11
+            np.testing.assert_allclose(g[b], og, atol=1e-11)

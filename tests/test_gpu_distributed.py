@@ -71,3 +71,26 @@ def test_two_ranks_on_one_gpu_match_single_process():
         np.testing.assert_allclose(gc, g, atol=1e-11)
         np.testing.assert_allclose(eb, v, atol=1e-11)
         np.testing.assert_allclose(gb, g, atol=1e-11)
+
+
+@pytest.mark.parametrize("config", ["cfg4", "cfg5"])
+def test_bench_gpus2_relaunch_matches_single_process(config):
+    """``bench.py --gpus 2`` re-launches itself as two ranks (torchrun); with
+    TQ_DIST_BACKEND=gloo both ranks share cuda:0.  Rank 0's line must report n_gpus 2 and the
+    chain-sharded energies/gradients (energy all-reduce + halo exchange + owned gather) must
+    match one process evaluating the whole operator (--check)."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TQ_DIST_BACKEND="gloo")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--batch", "4",
+           "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check"]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    par = line["parity"]
+    assert par["max_abs_dE"] < 1e-4, par
+    if par["max_abs_dgrad"] is not None:
+        assert par["max_abs_dgrad"] <= 1e-5 * max(par["max_abs_grad"], 1.0), par

@@ -17,7 +17,7 @@ from helpers_engine import grad_ok64, to_circuit, to_ham, tol64  # noqa: E402
 from paper_2112_10239_b200 import autodiff as AD  # noqa: E402
 from paper_2112_10239_b200 import chain as C  # noqa: E402
 from paper_2112_10239_b200.circuits import Circuit, standard_gate  # noqa: E402
-from paper_2112_10239_b200.errors import BondTooLarge, InputError, ParamCountMismatch  # noqa: E402
+from paper_2112_10239_b200.errors import BondTooLarge, InputError, ParamCountMismatch, TooManyQubits  # noqa: E402
 from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, term, tfim  # noqa: E402
 from paper_2112_10239_b200.workloads import CONFIGS, layered_circuit, theta_sets  # noqa: E402
 
@@ -141,9 +141,9 @@ def test_cfg4_energy_and_shift_coordinates(golden_large):
     v, g = AD.grad_expval(c, h, th)
     e_ref = float(golden_large["cfg4_E"])
     assert abs(v - e_ref) <= tol64(e_ref, h), (v, e_ref)
-    gnorm = max(np.max(np.abs(g)), 1.0)
+    gnorm = np.max(np.abs(g))
     for k, ref in zip(golden_large["cfg4_coords"], golden_large["cfg4_shift"]):
-        assert abs(g[k] - ref) <= 1e-5 * abs(ref) + 2e-6 * gnorm, (k, g[k], ref)
+        assert abs(g[k] - ref) <= 1e-5 * abs(ref) + 1e-6 * gnorm, (k, g[k], ref)
 
 
 def test_error_taxonomy():
@@ -153,7 +153,15 @@ def test_error_taxonomy():
     with pytest.raises(InputError):
         AD.grad_expval(c, tfim(4), np.full(4, np.nan))
     with pytest.raises(InputError):
-        AD.grad_expval(c, tfim(4), np.zeros(4), engine="dense")
+        AD.grad_expval(c, tfim(4), np.zeros(4), engine="mps")
+    # the reference's default engine seam: 'dense' gives the exact values (eps/chi_max ignored, as
+    # the reference's state-vector path ignores them) with the same 26-qubit guard
+    th = theta_sets(c.n_params, 1, seed=3)[0]
+    vd, gd = AD.grad_expval(c, tfim(4), th, engine="dense", dtype="complex128", eps=0.3, chi_max=1)
+    vt, gt = AD.grad_expval(c, tfim(4), th, engine="tt", dtype="complex128")
+    assert vd == vt and np.array_equal(gd, gt)
+    with pytest.raises(TooManyQubits):
+        AD.evaluate_expval(layered_circuit(27, 2), tfim(27), engine="dense")
     wide = Circuit(8, tuple(standard_gate("cnot", (0, 7)) for _ in range(6)), ())
     with pytest.raises(BondTooLarge):
         AD.evaluate_expval(wide, tfim(8), [])

@@ -83,3 +83,22 @@ def test_reading_a_generator_counts():
     assert c.n_params == 500 and len(c.gates) == 748
     c = O.brickwork(1024, 4)
     assert c.n_params == 8192 and len(c.gates) == 9727
+
+
+def test_oracle_adam_matches_reference_minimize():
+    """The oracle's Adam restatement (used by the f1 GPU checks) against the REAL reference's
+    minimize on mbe_objective (tests/golden/golden_f1.json): every iteration's loss to 1e-10."""
+    import json
+    import os
+
+    import oracle as O
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_f1.json")
+    case = [c for c in json.load(open(path))["cases"] if c["optimizer"] == "adam"][0]
+    n = (case["V"] + 1) // 2
+    fun = O.mbe_objective(O.brickwork(n, case["depth"]), case["V"], [tuple(e) for e in case["edges"]],
+                          alpha=case["alpha"])
+    run = case["runs"][0]
+    theta, values = O.adam_minimize(fun, np.array(run["theta0"]), rate=case["rate"], max_iters=case["max_iters"])
+    np.testing.assert_allclose(values, run["loss"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(theta, run["theta_final"], atol=1e-9)
