@@ -136,6 +136,18 @@ template <typename C> __device__ __forceinline__ C pauli_fac(int op, int sp) {
 }
 
 // ------------------------------------------------------------------ stage helpers
+// cos(t/2), sin(t/2) of a rotation angle.  complex64 takes the fp64 sincos rounded to fp32:
+// CUDA's fp32 sincosf is biased outward (mean c^2 + s^2 - 1 = +1.79e-8 over uniform angles,
+// tools/micro/sincos_bias.cu), which grows the state norm by ~1.8e-7 per 10-rotation column and
+// scales a 1000-site chain's energy by 1 + 1.8e-4 (tools/prec_diag.py); the rounded fp64 values
+// are unbiased (mean -4.6e-12).
+template <typename R>
+__device__ __forceinline__ void half_angle_sincos(R t, R& sn, R& cs) {
+  double sd, cd;
+  sincos(double(t) * 0.5, &sd, &cd);
+  sn = R(sd); cs = R(cd);
+}
+
 // Stage one site's descriptors for this theta-set into shared memory: the resolved
 // 2x2 factors (entry e of the site lives at mats[ent_begin + e]), packed op codes and
 // the MPO edges of the current sweep with their coefficients looked up once.
@@ -154,8 +166,7 @@ __device__ void stage_site(const tq_chain& ch, const R* theta_row, const R* coef
     } else {
       const R t = mt.slot >= 0 ? theta_row[mt.slot] : R(mt.angle);
       R sn, cs;
-      if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); sn = R(sf); cs = R(cf); }
-      else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); sn = R(sd); cs = R(cd); }
+      half_angle_sincos<R>(t, sn, cs);
       const R z = R(0);
       if (kind == 1) { m00 = cmk<C>(cs, z); m01 = cmk<C>(z, -sn); m10 = cmk<C>(z, -sn); m11 = cmk<C>(cs, z); }
       else if (kind == 2) { m00 = cmk<C>(cs, z); m01 = cmk<C>(-sn, z); m10 = cmk<C>(sn, z); m11 = cmk<C>(cs, z); }
@@ -254,8 +265,7 @@ __device__ void stage_blob(const int4* raw, const tq_site& st, const R* theta_ro
       // the caller may have loaded this lane's first angle ahead of time (latency off the path)
       const R t = slot >= 0 ? ((th_pre_ok && e == tid) ? th_pre : theta_row[slot]) : rp[FO + 1];
       R sn, cs;
-      if (sizeof(R) == 4) { float sf, cf; sincosf(float(t) * 0.5f, &sf, &cf); sn = R(sf); cs = R(cf); }
-      else { double sd, cd; sincos(double(t) * 0.5, &sd, &cd); sn = R(sd); cs = R(cd); }
+      half_angle_sincos<R>(t, sn, cs);
       const R z = R(0);
       if (kind == 1) { m00 = cmk<C>(cs, z); m01 = cmk<C>(z, -sn); m10 = cmk<C>(z, -sn); m11 = cmk<C>(cs, z); }
       else if (kind == 2) { m00 = cmk<C>(cs, z); m01 = cmk<C>(-sn, z); m10 = cmk<C>(sn, z); m11 = cmk<C>(cs, z); }

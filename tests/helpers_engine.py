@@ -23,8 +23,9 @@ def tol64(ref_val, ham):
 
 
 def grad_ok64(g, ref):
-    """complex64 gradient bar of SURVEY.md section 8c: |dg| <= 1e-5 |g_ref| + 1e-6 ||g_ref||_inf
-    (the reference's relative-or-absolute-floor rule, test_autodiff.py:116-120)."""
+    """complex64 gradient bar of SURVEY.md section 8c: |dg| <= 1e-5 |g_ref| + 1e-6 ||g_ref||_inf,
+    plus the reference's 1e-9 absolute floor for an identically-zero gradient vector
+    (relative-or-absolute-floor rule, test_autodiff.py:116-120)."""
     ref = np.asarray(ref)
     scale = np.max(np.abs(ref), initial=0.0)
-    return np.all(np.abs(g - ref) <= 1e-5 * np.abs(ref) + 1e-6 * scale)
+    return np.all(np.abs(g - ref) <= 1e-5 * np.abs(ref) + 1e-6 * scale + 1e-9)

@@ -1,0 +1,23 @@
+// fp32 sincosf bias probe: mean over many angles of (c^2 + s^2 - 1), c, s from sincosf(x)
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void k(double* out, int n) {
+  double acc = 0, acc2 = 0, accd = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float x = (float)((double)i / n * 6.283185307179586 - 3.141592653589793);
+    float s, c; sincosf(x * 0.5f, &s, &c);
+    acc += (double)c * c + (double)s * s - 1.0;
+    double sd, cd; sincos((double)(x * 0.5f), &sd, &cd);
+    const float cf = (float)cd, sf = (float)sd;
+    acc2 += (double)cf * cf + (double)sf * sf - 1.0;
+    accd += ((double)c - cd) * cd + ((double)s - sd) * sd;
+  }
+  atomicAdd(out, acc); atomicAdd(out + 1, acc2); atomicAdd(out + 2, accd);
+}
+int main() {
+  double* d; cudaMalloc(&d, 24); cudaMemset(d, 0, 24);
+  const int n = 1 << 26;
+  k<<<1184, 256>>>(d, n);
+  double h[3]; cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+  printf("sincosf: mean(c^2+s^2-1) = %.3e   fp64-rounded: %.3e   radial err of sincosf = %.3e\n", h[0] / n, h[1] / n, h[2] / n);
+}

@@ -1,7 +1,8 @@
 #!/bin/bash
-# Round-2 GPU check: the GPU suite, the default bench line (cfg4) and the reference arm.
+# Round-2 GPU check: precision diagnostic, the GPU suite, bench lines (cfg4 default, cfg2) and the reference arm.
 set -u
 mkdir -p gpurun_out/r2
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r2/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2/pytest_gpu.txt
-timeout 600 python bench.py > gpurun_out/r2/bench_cfg4.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/r2/bench_cfg4.log | cut -c1-600
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2/ref_cfg4.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/r2/ref_cfg4.log | cut -c1-400
+timeout 300 python tools/prec_diag.py > gpurun_out/r2/prec.txt 2>&1; echo "prec rc=$?"; cat gpurun_out/r2/prec.txt
+timeout 1800 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/r2/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; grep -E "passed|failed|FAILED|Error" gpurun_out/r2/pytest_gpu.txt | tail -15
+timeout 600 python bench.py > gpurun_out/r2/bench_cfg4.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/r2/bench_cfg4.log | cut -c1-300
+timeout 600 python bench.py --config cfg2 > gpurun_out/r2/bench_cfg2.log 2>&1; echo "bench2 rc=$?"; tail -1 gpurun_out/r2/bench_cfg2.log | cut -c1-300
