@@ -117,7 +117,9 @@ typedef struct {
   const void* blob;
   const int32_t* blob_off;    /* [n_sites] offset of each site's blob (16-byte units) */
   int32_t blob_max, blob_dtype; /* largest blob (units); dtype the entries were packed for */
-  int32_t max_pairs, pad2;      /* largest chi_l*chi_r of any site */
+  int32_t max_pairs;            /* largest chi_l*chi_r of any site */
+  int32_t max_ttree;            /* largest sum of trainable-op digit-tree levels (entries) of any column;
+                                   0 = unknown (the adjoint then sizes its kept levels by max_tree) */
 } tq_chain;
 
 /* Bytes of device workspace one call needs. */

@@ -41,7 +41,7 @@ class TqChain(ctypes.Structure):
         ("term_active", ctypes.c_void_p),
         ("blob", ctypes.c_void_p), ("blob_off", ctypes.c_void_p),
         ("blob_max", ctypes.c_int32), ("blob_dtype", ctypes.c_int32),
-        ("max_pairs", ctypes.c_int32), ("pad2", ctypes.c_int32),
+        ("max_pairs", ctypes.c_int32), ("max_ttree", ctypes.c_int32),
     ]
 
 
@@ -276,6 +276,7 @@ class DevicePlan:
         ch.blob_max = bmax
         ch.blob_dtype = code
         ch.max_pairs = int((plan.sites["chi_l"] * plan.sites["chi_r"]).max()) if len(plan.sites) else 1
+        ch.max_ttree = int(plan.max_ttree)
         self.chain = ch
         self._ws = {}
 

@@ -311,6 +311,7 @@ class ChainPlan:
     d_max: int
     max_edges: int
     max_tree: int
+    max_ttree: int        # largest sum of trainable-op tree levels of any column (compact adjoint tree)
     max_ops: int
     max_lmat: int
     max_train: int
@@ -370,7 +371,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
     sites, ops, mats, edges, fins, passes, segs = [], [], [], [], [], [], []
     mat_index = {}
     gred = {}  # theta slot -> list of absolute partial indices
-    chi_max, d_max, max_ops, max_lmat, max_train, max_tree = 1, 1, 0, 1, 0, 1
+    chi_max, d_max, max_ops, max_lmat, max_train, max_tree, max_ttree = 1, 1, 0, 1, 0, 1, 1
     env_total = 0
     gslot_total = 0
     init_vecs = None if init is None else np.asarray(init, dtype=complex).reshape(n, 2)
@@ -458,6 +459,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
             ntrain = 0
             toff = 0      # digit bits introduced before this op (digit-tree level index width)
             tbase = 0     # entries of all previous tree levels
+            ttb = 0       # entries of the previous trainable ops' levels (compact adjoint tree)
             for (src, shift, bits, specs) in col[q]:
                 o = np.zeros((), dtype=OP_DTYPE)
                 base = mat_block(specs)
@@ -475,10 +477,13 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
                     o["tidx"], o["gidx"] = -1, -1
                 o["toff"], o["tbase"] = toff, tbase
                 tbase += 1 << (toff + bits)
+                if o["tidx"] >= 0:
+                    ttb += 1 << (toff + bits)
                 toff += bits
                 lmat += 1 << bits
                 ops.append(o)
             max_tree = max(max_tree, tbase)
+            max_ttree = max(max_ttree, ttb)
             rec["op_count"] = len(col[q])
             rec["lmat_count"] = lmat
             rec["n_train"] = ntrain
@@ -534,7 +539,7 @@ def compile_chain(circuit, ham_terms, mode="energy", batch=1, segments=None, ini
         sites=arr(sites, SITE_DTYPE), ops=arr(ops, OP_DTYPE), mats=arr(mats, MAT_DTYPE),
         edges=arr(edges, EDGE_DTYPE), fins=arr(fins, EDGE_DTYPE), passes=arr(passes, PASS_DTYPE),
         segs=arr(segs, SEG_DTYPE), gred_ptr=ptr, gred_idx=np.array(idx, dtype=np.int32),
-        chi_max=chi_max, d_max=d_max, max_edges=_max_edges(sites), max_tree=max_tree, max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
+        chi_max=chi_max, d_max=d_max, max_edges=_max_edges(sites), max_tree=max_tree, max_ttree=max_ttree, max_ops=max_ops, max_lmat=max_lmat, max_train=max_train,
         n_gslots=gslot_total, env_total=env_total, e_const=e_const, term_active=active,
     )
     plan.info = {"segments": len(segs), "sub_chain_sites": int(sum(int(s["site_count"]) for s in segs)),

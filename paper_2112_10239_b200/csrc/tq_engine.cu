@@ -29,10 +29,6 @@
 
 #include "../../include/tq_engine.h"
 
-#ifndef FUSED_TC_DISABLED
-#define FUSED_TC_DISABLED 0
-#endif
-
 namespace tq {
 
 // ------------------------------------------------------------------ complex helpers
@@ -73,7 +69,6 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
                          // folded cores (A, A2 ping-pong) and P (dense) are cp.async-prefetched
   int32_t a2;            // second folded-core buffer (direct path)
   int32_t wc;            // fused path: per-site channel-pair 2x2 bracket matrices + nonzero mask
-  int32_t tc;            // chi = 32 tensor-core path: mbarrier + TMEM base address (16 B), or -1
   int32_t team_bytes;
 };
 
@@ -104,7 +99,6 @@ struct Params {
   double* values;   // [B][n_terms][2]
   int32_t store_env;
   int32_t mode;     // 0 energy-grad, 1 values
-  int32_t use_tc;             // chi = 32 products on tcgen05 (3xTF32), see tc_product
   const unsigned char* wct;   // per-(site, direction) bracket matrices built once per launch (or null)
   int32_t wct_row;            // bytes per table row
 };
@@ -421,81 +415,67 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
 }
 
 
-// ------------------------------------------------------------------ digit-tree column fold
+// ------------------------------------------------------------------ digit-tree column adjoint
 // The column's ops introduce bond digits one at a time, so after op l the distinct column
-// vectors are indexed by the digits introduced so far (toff_l + bits_l bits, the newest
-// digit on top).  Level l of the tree holds 2^(toff_l+bits_l) 2-vectors at lev[tbase_l];
-// the last level holds A[.][alpha][beta] at index idx(alpha, beta).  Cost per site is
-// sum_l 2^(bits so far) matvecs instead of chi_l*chi_r*L for per-pair walks.
+// vectors are indexed by the digits introduced so far (toff_l + bits_l bits, the newest digit
+// on top): level l holds 2^(toff_l+bits_l) 2-vectors, and the last level is A[.][alpha][beta]
+// at index idx(alpha, beta).  Cost per column: sum_l 2^(bits so far) matvecs instead of
+// chi_l*chi_r*L for per-pair walks.
+//
+// Compact storage (adj_sweep, chi >= 16): the adjoint reads a forward level V_l only at a
+// trainable op, so only those levels are kept (levt, at per-op offsets tbase[oi]); the others
+// ping-pong through two scratch buffers of 2^(bits) vectors, which the backward walk then reuses
+// for U.  cfg4: 16 KB of kept levels instead of 49 KB for all of them, so four 128-thread units
+// fit on an SM.
 template <typename R, int TEAM>
-__device__ void tree_forward(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
-                             const int* obase, typename CT<R>::T* lev) {
+__device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
+                              typename CT<R>::T* levt, typename CT<R>::T* buf0, typename CT<R>::T* buf1,
+                              int* tbase) {
   using C = typename CT<R>::T;
   const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+  const C* src = nullptr;   // null: the initial vector
+  int tb = 0;
   for (int oi = 0; oi < st.op_count; ++oi) {
     const int c = ocode[oi];
     const int toff = oc_toff(c), nn = 1 << (toff + oc_bits(c));
-    const int base = obase[oi], pbase = oi ? obase[oi - 1] : 0;
+    C* dst;
+    if (oc_tidx(c) >= 0) {
+      dst = levt + 2 * tb;
+      if (tid == 0) tbase[oi] = tb;
+      tb += nn;
+    } else {
+      dst = src == buf0 ? buf1 : buf0;   // never the level being read
+    }
     const C* Mb = mres + 4 * oc_lmat(c);
     for (int e = tid; e < nn; e += TEAM) {
       const int idx = e & ((1 << toff) - 1);
       const C* M = Mb + 4 * (e >> toff);
-      const C v0 = oi ? lev[2 * (pbase + idx)] : i0;
-      const C v1 = oi ? lev[2 * (pbase + idx) + 1] : i1;
+      const C v0 = src ? src[2 * idx] : i0;
+      const C v1 = src ? src[2 * idx + 1] : i1;
       C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
       C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
-      lev[2 * (base + e)] = n0; lev[2 * (base + e) + 1] = n1;
+      dst[2 * e] = n0; dst[2 * e + 1] = n1;
     }
     team_sync<TEAM>();
+    src = dst;
   }
 }
 
-__device__ __forceinline__ int tree_index(const int* ocode, int nops, int al, int be) {
-  int idx = 0;
-  for (int oi = 0; oi < nops; ++oi) {
-    const int c = ocode[oi];
-    if (oc_bits(c)) idx |= oc_digit(c, al, be) << oc_toff(c);
-  }
-  return idx;
-}
-
-// A[s] / AH[s] from the last tree level (zero where passthrough digits disagree).
-template <typename R, int LD, int TEAM>
-__device__ void tree_scatter(const tq_chain& ch, const tq_site& st, int tid, const int* ocode, const int* obase,
-                             const typename CT<R>::T* lev, typename CT<R>::T* A, typename CT<R>::T* AH, int lcr) {
+// Column adjoint on the compact tree: U_last[idx] = sum over passthrough-matched (alpha, beta)
+// of the core cotangent (G[0], G[1])[alpha][beta] (read straight from HBM, dense [2][cl][cr]);
+// walking down, every trainable rotation accumulates Im<U_l, sigma V_l> (per-warp partials in
+// contrib) and U_{l-1}[idx] = sum_d M_l(d)^H U_l[idx | d << toff_l].
+template <typename R, int TEAM>
+__device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                              const int* minfo, const int* ocode, const typename CT<R>::T* levt, const int* tbase,
+                              typename CT<R>::T* ua, typename CT<R>::T* ub, const typename CT<R>::T* gg, int lcr,
+                              R* contrib) {
   using C = typename CT<R>::T;
-  const int npair = st.chi_l * st.chi_r;
-  const int last = st.op_count - 1;
-  const int lbase = last >= 0 ? obase[last] : 0;
-  for (int pi = tid; pi < npair; pi += TEAM) {
-    const int al = pi >> lcr, be = pi & (st.chi_r - 1);
-    C v0, v1;
-    if (st.pass_count && !pass_ok(ch, st, al, be)) { v0 = cmk<C>(R(0), R(0)); v1 = v0; }
-    else if (last < 0) { v0 = cmk<C>(R(st.init[0]), R(st.init[1])); v1 = cmk<C>(R(st.init[2]), R(st.init[3])); }
-    else {
-      const int idx = tree_index(ocode, st.op_count, al, be);
-      v0 = lev[2 * (lbase + idx)]; v1 = lev[2 * (lbase + idx) + 1];
-    }
-    A[al * LD + be] = v0; A[LD * LD + al * LD + be] = v1;
-    if (AH) { AH[be * LD + al] = cconj(v0); AH[LD * LD + be * LD + al] = cconj(v1); }
-  }
-}
-
-// Column adjoint on the digit tree: U_last[idx] = sum over passthrough-matched (alpha, beta)
-// of (G[0], G[1])[alpha][beta]; walking down, every trainable rotation accumulates
-// Im<U_l, sigma V_l> and U_{l-1}[idx] = sum_d M_l(d)^H U_l[idx | d << toff_l].
-template <typename R, int LD, int TEAM>
-__device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
-                             const int* minfo, const int* ocode, const int* obase, const typename CT<R>::T* lev,
-                             typename CT<R>::T* ubuf, const typename CT<R>::T* G, R* contrib) {
-  using C = typename CT<R>::T;
-  constexpr int MS = LD * LD;
   const int nops = st.op_count;
   if (nops == 0) return;
+  const int np = st.chi_l * st.chi_r;
   const int clast = ocode[nops - 1];
   const int nlast = 1 << (oc_toff(clast) + oc_bits(clast));
-  C* ua = ubuf;
-  C* ub = ubuf + 2 * nlast;
   int npb = 0;
   for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
   for (int e = tid; e < nlast; e += TEAM) {
@@ -516,7 +496,7 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
         const int v = (cmb >> used) & ((1 << ps.bits) - 1);
         a2 |= v << ps.sa; b2 |= v << ps.sb; used += ps.bits;
       }
-      const C x0 = G[a2 * LD + b2], x1 = G[MS + a2 * LD + b2];
+      const C x0 = gg[(a2 << lcr) + b2], x1 = gg[np + (a2 << lcr) + b2];
       g0.x += x0.x; g0.y += x0.y; g1.x += x1.x; g1.y += x1.y;
     }
     ua[2 * e] = g0; ua[2 * e + 1] = g1;
@@ -527,13 +507,12 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
     const int toff = oc_toff(c), bits = oc_bits(c);
     const int nn = 1 << (toff + bits);
     const int tix = oc_tidx(c);
-    const C* V = lev + 2 * obase[oi];
     const int lm = oc_lmat(c);
     if (tix >= 0) {
+      const C* V = levt + 2 * tbase[oi];
       R acc = R(0);
       for (int e = tid; e < nn; e += TEAM) {
-        const int ent = lm + (e >> toff);
-        const int kind = minfo[ent] & 0xff;
+        const int kind = minfo[lm + (e >> toff)] & 0xff;
         if (kind == 0) continue;
         const C u0 = ua[2 * e], u1 = ua[2 * e + 1];
         const C v0 = V[2 * e], v1 = V[2 * e + 1];
@@ -550,8 +529,8 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
       if ((tid & 31) == 0) contrib[tix * (TEAM / 32) + (tid >> 5)] += acc;   // per-warp partials
     }
     if (oi > 0) {
-      const int np = 1 << toff;
-      for (int idx = tid; idx < np; idx += TEAM) {
+      const int npv = 1 << toff;
+      for (int idx = tid; idx < npv; idx += TEAM) {
         C w0 = cmk<C>(R(0), R(0)), w1 = w0;
         for (int d = 0; d < (1 << bits); ++d) {
           const C* M = mres + 4 * (lm + d);
@@ -566,7 +545,6 @@ __device__ void tree_adjoint(const tq_chain& ch, const tq_site& st, int tid, con
   }
   team_sync<TEAM>();
 }
-
 
 
 // Warp-direct variant for one pair per lane (warp teams): every lane walks its pair (zero
@@ -815,6 +793,57 @@ __device__ __forceinline__ void bracket_stage(int tid, int ntarget, int ec, cons
   }
 }
 
+// The same bracket from the site's channel-pair 2x2 matrices W_(src,tgt)[s'][s] (built once per
+// launch by build_wct, or per site by stage_blob): every thread owns two (i, j) elements and
+// forms all (target, s') outputs from all (source, s) inputs in registers, skipping channel pairs
+// the mask marks empty.  chi >= 16 (the per-edge loop of bracket_stage is latency bound there).
+template <typename R, int LD, int TEAM, int DM>
+__device__ __forceinline__ void wbracket_stage(int tid, int nsrc, int ntgt, const typename CT<R>::T* SRC,
+                                               const typename CT<R>::T* wc, typename CT<R>::T* BR, int lcl, int lcr) {
+  using C = typename CT<R>::T;
+  constexpr int MS = LD * LD;
+  constexpr int U = 2;
+  const int wmask = reinterpret_cast<const int*>(wc + 4 * DM * DM)[0];
+  const int nel = 1 << (lcl + lcr);
+  for (int e0 = tid; e0 < nel; e0 += TEAM * U) {
+    int off[U];
+    bool on[U];
+    C v[U][DM][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * TEAM;
+      on[u] = e < nel;
+      off[u] = on[u] ? (e >> lcr) * LD + (e & ((1 << lcr) - 1)) : 0;
+#pragma unroll
+      for (int x = 0; x < DM; ++x)
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+          v[u][x][s] = (x < nsrc && on[u]) ? SRC[(x * 2 + s) * MS + off[u]] : cmk<C>(R(0), R(0));
+    }
+#pragma unroll
+    for (int xt = 0; xt < DM; ++xt) {
+      if (xt >= ntgt) continue;
+      C o[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) { o[u][0] = cmk<C>(R(0), R(0)); o[u][1] = o[u][0]; }
+#pragma unroll
+      for (int xs = 0; xs < DM; ++xs) {
+        if (!((wmask >> (xs * DM + xt)) & 1)) continue;
+        const C* w = wc + 4 * (xs * DM + xt);
+        const C w00 = w[0], w01 = w[1], w10 = w[2], w11 = w[3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cfma(o[u][0], w00, v[u][xs][0]); cfma(o[u][0], w01, v[u][xs][1]);
+          cfma(o[u][1], w10, v[u][xs][0]); cfma(o[u][1], w11, v[u][xs][1]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (on[u]) { BR[(xt * 2 + 0) * MS + off[u]] = o[u][0]; BR[(xt * 2 + 1) * MS + off[u]] = o[u][1]; }
+    }
+  }
+}
+
 // Rows per item for the fused product+bracket stages: enough items for every thread.
 __device__ __forceinline__ int fused_rows(int m, int nel, int team, int rtmax) {
   int rt = nel / team;
@@ -939,119 +968,6 @@ __device__ __forceinline__ void store_rows(C* o, int rt, C a0, C a1, C a2, C a3)
   if (rt > 2) { o[2 * LD] = a2; o[3 * LD] = a3; }
 }
 
-// ------------------------------------------------------------------ tcgen05 (chi = 32, complex64)
-// N[b][s] = A[s] P[b] for all (b, s) of a 32 x 32 site as ONE real-embedded tensor-core product:
-//   D'[(s, part, i), (b, j)] = sum_{(q, k)} A'[(s, part, i), (q, k)] B'[(b, j), (q, k)]
-// with A' = [[Ar, -Ai], [Ai, Ar]] per spin (M' = 128 rows), B' = [Pr; Pi] (K' = 64), N' = 32 db.
-// 3xTF32: big*big + big*small + small*big accumulate in TMEM (fp32-level accuracy for the
-// 1e-5 parity bar).  Operands are K-major SWIZZLE_NONE core matrices (8 rows x 16 B) staged in
-// the N/BR slots, which are dead until this product's epilogue writes N.
-__device__ __forceinline__ uint32_t smem_addr_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-__device__ __forceinline__ int kmaj_off(int row, int k) {   // floats; K' = 64: SBO = 16 core matrices
-  return (row >> 3) * 512 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
-}
-__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(2048 >> 4) << 32) |
-         ((uint64_t)1 << 46);
-}
-__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-               :: "r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void tc_commit_wait(uint64_t* mbar, uint32_t& phase, int tid) {
-  if (tid == 0) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" :: "r"(smem_addr_u32(mbar)));
-  asm volatile("{\n\t.reg .pred done;\n\tTQ_TC_WAIT:\n\t"
-               "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-               "@!done bra TQ_TC_WAIT;\n\t}\n" :: "r"(smem_addr_u32(mbar)), "r"(phase) : "memory");
-  phase ^= 1u;
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-}
-
-template <int TEAM>
-__device__ void tc_product(int tid, int db, const float2* A, const float2* P, float2* N, float* ops,
-                           uint64_t* mbar, uint32_t tmem, uint32_t& phase) {
-  constexpr int LD = 33, MS = LD * LD;
-  const int np = db * 32;          // N'
-  float* Ab = ops;                 // 128 x 64
-  float* Bb = ops + 128 * 64;      // np x 64
-  float* Bs = Bb + np * 64;        // np x 64  (make_layout reserves 128 B + 32 KB + 2 x 8 KB per channel)
-  // stage big parts of A' and B', small parts of B'.  Threads walk the destination (core-matrix)
-  // order, so the shared stores are conflict-free; the reads gather from the LD-padded sources.
-  for (int d = tid; d < 128 * 64; d += TEAM) {
-    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
-    const int sp = row >> 6, part = (row >> 5) & 1, i = row & 31, q = kq >> 5, k = kq & 31;
-    const float2 a = A[sp * MS + i * LD + k];
-    const float v = part == 0 ? (q == 0 ? a.x : -a.y) : (q == 0 ? a.y : a.x);
-    Ab[d] = tf32_rna(v);
-  }
-  for (int d = tid; d < np * 64; d += TEAM) {
-    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
-    const int bb = row >> 5, j = row & 31, q = kq >> 5, k = kq & 31;
-    const float2 pv = P[bb * MS + k * LD + j];
-    const float v = q == 0 ? pv.x : pv.y;
-    const float hb = tf32_rna(v);
-    Bb[d] = hb;
-    Bs[d] = tf32_rna(v - hb);
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  team_sync<TEAM>();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint32_t aA = smem_addr_u32(Ab), aB = smem_addr_u32(Bb), aS = smem_addr_u32(Bs);
-  if (tid == 0) {
-#pragma unroll 1
-    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aB + ks * 256), idesc, ks > 0);
-#pragma unroll 1
-    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aS + ks * 256), idesc, 1u);
-  }
-  tc_commit_wait(mbar, phase, tid);
-  // small part of A' over the big part (its MMAs have completed)
-  for (int d = tid; d < 128 * 64; d += TEAM) {
-    const int row = ((d >> 9) << 3) | ((d >> 2) & 7), kq = (((d >> 5) & 15) << 2) | (d & 3);
-    const int sp = row >> 6, part = (row >> 5) & 1, i = row & 31, q = kq >> 5, k = kq & 31;
-    const float2 a = A[sp * MS + i * LD + k];
-    const float v = part == 0 ? (q == 0 ? a.x : -a.y) : (q == 0 ? a.y : a.x);
-    Ab[d] = tf32_rna(v - tf32_rna(v));
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  team_sync<TEAM>();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (tid == 0) {
-#pragma unroll 1
-    for (int ks = 0; ks < 8; ++ks) tc_mma(tmem, umma_desc(aA + ks * 256), umma_desc(aB + ks * 256), idesc, 1u);
-  }
-  tc_commit_wait(mbar, phase, tid);
-  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (rows (s, part, i)), columns of group w / 4
-  const int warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, sp = q >> 1, part = q & 1;
-  const int ngrp = TEAM / 128;                 // warps sharing a lane quarter
-  const int per = np / ngrp;                   // columns per warp (multiple of 8)
-  const int c0 = (warp >> 2) * per;
-  for (int cc = 0; cc < per; cc += 8) {
-    uint32_t v[8];
-    const uint32_t addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c0 + cc);
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int c = c0 + cc + t, bb = c >> 5, j = c & 31;
-      float* dst = reinterpret_cast<float*>(N + (bb * 2 + sp) * MS + lane * LD + j);
-      dst[part] = __uint_as_float(v[t]);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-}
-
 // Row of the launch's bracket-matrix table for (site, direction), or null (built in the sweep).
 template <typename C>
 __device__ __forceinline__ const C* wct_row_of(const Params& p, int site, int dir) {
@@ -1069,9 +985,10 @@ rl_sweep(Params p) {
   constexpr int LD = CHI + 1;
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
-  constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
-  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
-  constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
+  constexpr bool FUSE = FD > 0 && CHI <= 8;       // register-fused product+bracket (host: chi <= 8 && D <= FD)
+  constexpr bool WBR = FD > 0 && CHI >= 16;       // unfused GEMMs, matrix bracket (host: chi >= 16 && D <= FD)
+  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused / matrix-bracket stages
+  constexpr int DMW = (FUSE || WBR) ? FDM : 0;    // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
@@ -1111,28 +1028,6 @@ rl_sweep(Params p) {
     team_sync<TEAM>();
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
   }
-  // chi = 32 complex64: the A[s] P[b] products run on tcgen05 (one CTA = one team)
-  constexpr bool TCK = CHI == 32 && sizeof(R) == 4 && TEAM == 512 && !FUSED_TC_DISABLED;
-  const bool use_tc = TCK && p.use_tc && p.L.tc >= 0;
-  uint64_t* tc_mbar = nullptr;
-  uint32_t tc_tmem = 0, tc_phase = 0;
-  if constexpr (TCK) {
-    if (use_tc) {
-      unsigned char* tcb = smem_raw + p.L.tc;
-      tc_mbar = reinterpret_cast<uint64_t*>(tcb);
-      uint32_t* tslot = reinterpret_cast<uint32_t*>(tcb + 8);
-      if (tid < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
-                     :: "r"(smem_addr_u32(tslot)), "n"(128));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-      }
-      if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_addr_u32(tc_mbar)));
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      team_sync<TEAM>();
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      tc_tmem = *tslot;
-    }
-  }
   int cur = 0;
   for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
     team_sync<TEAM>();
@@ -1143,6 +1038,8 @@ rl_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
     STAGE(0);
+    // per-pair column walks: the digit-tree fold (levels in the dead N/BR slots) was measured
+    // slower at chi = 32 (11.7k vs 7.7k cycles per site: 20 team barriers over small levels)
     fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
@@ -1162,45 +1059,14 @@ rl_sweep(Params p) {
       STAGE(2);
     } else {
       // N[b][s] = A[s] * P[b]
-      bool done_tc = false;
-      if constexpr (TCK) {
-        if (use_tc && cl == 32 && cr == 32 && p.use_tc != 2) {
-          float* ops = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(N) + 127) & ~uintptr_t(127));
-          tc_product<TEAM>(tid, db, reinterpret_cast<const float2*>(sm.A), reinterpret_cast<const float2*>(PIN),
-                           reinterpret_cast<float2*>(N), ops, tc_mbar, tc_tmem, tc_phase);
-          done_tc = true;
-#ifdef TQ_TC_CHECK
-          team_sync<TEAM>();
-          gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-              [&](int t, int) { return sm.A + (t & 1) * MS; },
-              [&](int t, int) { return PIN + (t >> 1) * MS; },
-              [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(sm.BR + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
-          team_sync<TEAM>();
-          for (int e = tid; e < db * 2 * 1024; e += TEAM) {
-            const int t = e >> 10, i = (e >> 5) & 31, j = e & 31;
-            const C x = N[t * MS + i * LD + j], y = sm.BR[t * MS + i * LD + j];
-            if (fabsf(x.x - y.x) + fabsf(x.y - y.y) > 1e-5f)
-              printf("TCCHK blk=%d site q=%d db=%d t=%d i=%d j=%d tc=(%g,%g) simt=(%g,%g)\n", (int)blockIdx.x, q, db, t, i, j, x.x, x.y, y.x, y.y);
-          }
-          if (p.use_tc == 3) {
-            gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-                [&](int t, int) { return sm.A + (t & 1) * MS; },
-                [&](int t, int) { return PIN + (t >> 1) * MS; },
-                [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
-            team_sync<TEAM>();
-          }
-          team_sync<TEAM>();
-#endif
-        }
-      }
-      if (!done_tc)
-        gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+      gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
             [&](int t, int) { return sm.A + (t & 1) * MS; },
             [&](int t, int) { return PIN + (t >> 1) * MS; },
             [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
-      bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
+      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM>(tid, db, da, N, WC, sm.BR, lcl, lcr);
+      else bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
       blob_wait();
       team_sync<TEAM>();
       STAGE(3);
@@ -1233,13 +1099,6 @@ rl_sweep(Params p) {
     if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
   }
   if (tid == 0) reinterpret_cast<C*>(p.epart)[(size_t)b * S + g] = PIN[0];
-  if constexpr (TCK) {
-    if (use_tc) {
-      team_sync<TEAM>();
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tc_tmem), "n"(128));
-    }
-  }
   STAGE_END(0);
 }
 
@@ -1254,9 +1113,10 @@ lr_sweep(Params p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
-  constexpr bool FUSE = FD > 0;                   // register-fused product+bracket (host: chi <= 8 && D <= FD)
-  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused stages
-  constexpr int DMW = FUSE ? FDM : 0;             // channel-pair bracket matrices staged with the descriptors
+  constexpr bool FUSE = FD > 0 && CHI <= 8;       // register-fused product+bracket (host: chi <= 8 && D <= FD)
+  constexpr bool WBR = FD > 0 && CHI >= 16;       // unfused GEMMs, matrix bracket (host: chi >= 16 && D <= FD)
+  constexpr int FDM = FD > 0 ? FD : 4;            // channels handled by the fused / matrix-bracket stages
+  constexpr int DMW = (FUSE || WBR) ? FDM : 0;    // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int team = threadIdx.x / TEAM;
@@ -1368,7 +1228,8 @@ lr_sweep(Params p) {
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
-      bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
+      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM>(tid, da, db, M, WC, sm.BR, lcl, lcr);
+      else bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
       blob_wait();
       team_sync<TEAM>();
       STAGE(3);
@@ -1494,6 +1355,7 @@ lr_sweep(Params p) {
 // the left-to-right sweep's sequential critical path.
 struct AdjLayout {
   int32_t g, mres, minfo, mps, ocode, ogidx, obase, sbuf, raw, lev, ubuf, contrib, team_bytes, tree;
+  int32_t ubuf_vec;   // 2-vectors per U / scratch buffer of the compact digit tree
 };
 
 // Min resident 128-thread adjoint CTAs per SM (team-of-32 path).  6 measured best
@@ -1503,7 +1365,7 @@ struct AdjLayout {
 #define TQ_ADJ_MINB 6
 #endif
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : 1)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : (TEAM == 128 ? 4 : 1))
 adj_sweep(Params p, AdjLayout A) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
@@ -1557,10 +1419,11 @@ adj_sweep(Params p, AdjLayout A) {
     return;
   }
   stage_blob<R, TEAM>(raw, st, theta_b, nullptr, true, tid, mres, minfo, mps, ocode, ogidx, obase, nullptr, sbuf);
-  for (int e = tid; e < 2 * np; e += TEAM) {
-    const int sidx = e >= np, r = e - sidx * np;
-    Gs[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))] = gg[e];
-  }
+  if (!A.tree)   // per-pair walks read G from shared memory; the digit tree reads it from HBM once
+    for (int e = tid; e < 2 * np; e += TEAM) {
+      const int sidx = e >= np, r = e - sidx * np;
+      Gs[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))] = gg[e];
+    }
   const int ntr = st.n_train;
   R* contrib = reinterpret_cast<R*>(base + A.contrib);
   const int cw = A.tree ? TEAM / 32 : TEAM;
@@ -1569,9 +1432,11 @@ adj_sweep(Params p, AdjLayout A) {
   if constexpr (CHI >= 16) {
     if (A.tree) {
       C* lev = reinterpret_cast<C*>(base + A.lev);
-      C* ubuf = reinterpret_cast<C*>(base + A.ubuf);
-      tree_forward<R, TEAM>(st, tid, mres, ocode, obase, lev);
-      tree_adjoint<R, LD, TEAM>(p.c, st, tid, mres, minfo, ocode, obase, lev, ubuf, Gs, contrib);
+      C* u0 = reinterpret_cast<C*>(base + A.ubuf);
+      C* u1 = u0 + 2 * (A.ubuf_vec);
+      int* tbase = obase;   // host tbase offsets are for the full tree; the compact ones go here
+      ctree_forward<R, TEAM>(st, tid, mres, ocode, lev, u0, u1, tbase);
+      ctree_adjoint<R, TEAM>(p.c, st, tid, mres, minfo, ocode, lev, tbase, u0, u1, gg, lcr, contrib);
     }
   }
   const bool one_pair = np <= TEAM;
@@ -1800,19 +1665,6 @@ static void set_smem_attr(const void* fn, size_t smem) {
   if (used < 256) { keys[used] = fn; devs[used] = dev; vals[used] = smem; ++used; }
 }
 
-// chi = 32 complex64 products on tcgen05 (tc_product): opt-in with TQ_TC=1.  Correct (the GPU
-// parity suite passes with it on) but not yet faster: restaging the operands into the UMMA
-// layout with the 3xTF32 split costs as much as the FFMA product it replaces (cfg4 RL 10.7 vs
-// 9.7 ms).  The producers (fold, P epilogue) must emit UMMA-layout operands directly.
-static int tc_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TQ_TC");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 512); }
 static int chi_bucket(int chi) { int c = 2; while (c < chi) c <<= 1; return c; }
 
@@ -1827,24 +1679,20 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   const int D = c->d_max < 1 ? 1 : c->d_max;
   size_t off = 0;
   const bool fused = chi <= 8 && D <= 4 && (!lr || mode == 0);   // kernels: FUSE && D <= FDM
+  const bool wbr = chi >= 16 && D <= 4 && (!lr || mode == 0);     // kernels: WBR (matrix bracket, chi >= 16)
   L.direct = (lr && mode == 0 && fused && team == 32 && c->max_pairs <= 32 && c->max_ops <= 12) ? 1 : 0;
   L.a = (int32_t)off; off += 2 * ms;
   L.ah = L.a;                                        // conjugate transposes are read in place
   L.env = (int32_t)off; off += (size_t)D * ms;       // RL: P in/out; LR: Lambda
   L.m = (int32_t)off; off += (size_t)(fused ? (lr && !L.direct ? 2 : 0) : 2 * D) * ms;   // RL: N; LR: M (G aliases)
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
-  if (chi == 32 && rsz == 4 && !lr && !fused) {
-    // tcgen05 operands (tc_product) alias the N and BR slots: alignment + A' + B' big/small
-    const size_t need = 128 + (size_t)128 * 64 * 4 + (size_t)2 * 32 * D * 64 * 4;
-    if (off - (size_t)L.m < need) off = (size_t)L.m + need;
-  }
   L.pin = (int32_t)off;
   if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
   L.a2 = (int32_t)off;
   if (L.direct) off += 2 * ms;
   off = align_up(off, 16);
   L.wc = (int32_t)off;
-  if (fused) { const int dm = D <= 3 ? 3 : 4; off += align_up((size_t)dm * dm * 4 * csz + 16, 16); }
+  if (fused || wbr) { const int dm = D <= 3 ? 3 : 4; off += align_up((size_t)dm * dm * 4 * csz + 16, 16); }
   L.mr = (int32_t)off;
   if (lr && mode == 1) off += (size_t)2 * D * ms;
   // digit tree (gradient sweep, chi >= 16): per-warp contribution partials; adjoint
@@ -1882,8 +1730,6 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
       if (lev_bytes + u_bytes <= avail) { L.tree = 2; L.lev = (int32_t)(L.m + 2 * ms); L.ubuf = (int32_t)(L.lev + lev_bytes); }
     }
   }
-  L.tc = -1;
-  if (chi == 32 && rsz == 4 && !lr) { off = align_up(off, 16); L.tc = (int32_t)off; off += 16; }
   L.team_bytes = (int32_t)align_up(off, 128);
   return L;
 }
@@ -1909,13 +1755,14 @@ static WsLayout ws_layout(const tq_chain* c, int batch, int flags, int dtype) {
 struct Timing { cudaEvent_t ev[6]; bool on; };
 static thread_local Timing g_timing = {{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}, false};
 
+// Adjoint teams (launch_pair_f): a warp per (theta-set, site) up to chi = 8, 128 threads from
+// chi = 16 (four units per SM at cfg4 with the compact digit tree).
 static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rsz) {
   AdjLayout A{};
   const size_t csz = 2 * rsz;
   const size_t ms = (size_t)(chi + 1) * (chi + 1) * csz;
   size_t off = 0;
   auto take = [&](size_t bytes) { const int32_t o = (int32_t)off; off = align_up(off + bytes, 16); return o; };
-  A.g = take(2 * ms);
   A.mres = take((size_t)c->max_lmat * 4 * csz);
   A.minfo = take((size_t)c->max_lmat * 4);
   A.mps = take((size_t)c->max_lmat * rsz);
@@ -1926,15 +1773,19 @@ static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rs
   const int ntr = c->max_train > 0 ? c->max_train : 1;
   const size_t budget = (size_t)227 * 1024 / (team == 32 ? 4 : 1);
   A.tree = 0;
+  A.ubuf_vec = chi * chi;
   if (chi >= 16) {
-    const size_t lev = (size_t)(c->max_tree > 0 ? c->max_tree : 1) * 2 * csz;
-    const size_t ub = (size_t)2 * chi * chi * 2 * csz;
+    // compact digit tree: kept (trainable) levels + two buffers of chi^2 2-vectors; G is read
+    // from HBM, so no G slab
+    const int kept = c->max_ttree > 0 ? c->max_ttree : (c->max_tree > 0 ? c->max_tree : 1);
+    const size_t lev = (size_t)kept * 2 * csz;
+    const size_t ub = (size_t)2 * A.ubuf_vec * 2 * csz;
     const size_t ctb = (size_t)ntr * (team / 32) * rsz;
     if (align_up(off + lev + ub + ctb + 64, 128) <= budget) {
       A.tree = 1; A.lev = take(lev); A.ubuf = take(ub); A.contrib = take(ctb);
     }
   }
-  if (!A.tree) A.contrib = take((size_t)ntr * team * rsz);
+  if (!A.tree) { A.g = take(2 * ms); A.contrib = take((size_t)ntr * team * rsz); }
   A.team_bytes = (int32_t)align_up(off, 128);
   return A;
 }
@@ -1974,13 +1825,15 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
     if (prm.mode == 0) {
-      AdjLayout A = make_adj_layout(&prm.c, CHI, TEAM, sizeof(R));
-      const size_t asmem = (size_t)A.team_bytes * TEAMS;
+      constexpr int ATEAM = CHI <= 8 ? 32 : 128;   // adj_team_for_chi
+      constexpr int ATEAMS = ATEAM == 32 ? 4 : 1;
+      AdjLayout A = make_adj_layout(&prm.c, CHI, ATEAM, sizeof(R));
+      const size_t asmem = (size_t)A.team_bytes * ATEAMS;
       if (asmem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "adjoint shared-memory layout exceeds 227 KB");
       const int64_t units = (int64_t)prm.batch * prm.c.n_sites;
-      set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, TEAM>), asmem);
+      set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM>), asmem);
       if (g_timing.on) cudaEventRecord(g_timing.ev[4], s);
-      adj_sweep<R, CHI, TEAM><<<(unsigned)((units + TEAMS - 1) / TEAMS), TEAM * TEAMS, asmem, s>>>(prm, A);
+      adj_sweep<R, CHI, ATEAM><<<(unsigned)((units + ATEAMS - 1) / ATEAMS), ATEAM * ATEAMS, asmem, s>>>(prm, A);
       if (g_timing.on) cudaEventRecord(g_timing.ev[5], s);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
@@ -1993,12 +1846,11 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
 // shared-memory layout in make_layout makes the same decision).
 template <typename R, int CHI>
 static tq_status launch_pair(Params& prm, bool run_lr, cudaStream_t s) {
-  // chi >= 16: the register-fused stages were measured slower than GEMM + bracket
-  // (profiles/r01_stages_cfg4.txt), so they stay unfused
-  if constexpr (CHI <= 8) {
-    if (prm.c.d_max <= 3) return launch_pair_f<R, CHI, 3>(prm, run_lr, s);
-    if (prm.c.d_max <= 4) return launch_pair_f<R, CHI, 4>(prm, run_lr, s);
-  }
+  // chi <= 8: register-fused product + bracket.  chi >= 16: the fused stages were measured
+  // slower than GEMM + bracket (profiles/r01_stages_cfg4.txt); the GEMMs stay unfused and the
+  // bracket uses the same channel-pair matrices (wbracket_stage)
+  if (prm.c.d_max <= 3) return launch_pair_f<R, CHI, 3>(prm, run_lr, s);
+  if (prm.c.d_max <= 4) return launch_pair_f<R, CHI, 4>(prm, run_lr, s);
   return launch_pair_f<R, CHI, 0>(prm, run_lr, s);
 }
 
@@ -2011,8 +1863,8 @@ static tq_status dispatch(Params& prm, bool run_lr, cudaStream_t s) {
     case 8: return launch_pair<R, 8>(prm, run_lr, s);
     case 16: return launch_pair<R, 16>(prm, run_lr, s);
     case 32:
-      if (sizeof(R) == 8) return fail(TQ_ERR_UNSUPPORTED, "complex128 mode supports bond dimension <= 16");
-      return launch_pair<R, 32>(prm, run_lr, s);
+      if constexpr (sizeof(R) == 8) return fail(TQ_ERR_UNSUPPORTED, "complex128 mode supports bond dimension <= 16");
+      else return launch_pair<R, 32>(prm, run_lr, s);
     default: return fail(TQ_ERR_UNSUPPORTED, "bond dimension exceeds 32");
   }
 }
@@ -2037,12 +1889,11 @@ static tq_status energy_grad_impl(const tq_chain* c, int batch, const void* thet
   prm.c = *c; prm.batch = batch; prm.theta = theta; prm.theta_stride = ts; prm.coef = coef; prm.coef_stride = cs;
   prm.env = wb + w.env; prm.epart = wb + w.epart; prm.gpart = wb + w.gpart; prm.values = nullptr;
   prm.store_env = grad ? 1 : 0; prm.mode = 0;
-  prm.use_tc = tc_enabled();
   prm.wct = nullptr; prm.wct_row = (int32_t)w.wct_row;
   if (batch == 0) return TQ_OK;
   // one coefficient row for the whole batch + fused small-chi sweeps: build the bracket
   // matrices once per launch instead of once per (theta-set, site)
-  if (cs == 0 && coef != nullptr && c->n_sites > 0 && chi_bucket(c->chi_max) <= 8 && c->d_max <= 4) {
+  if (cs == 0 && coef != nullptr && c->n_sites > 0 && c->d_max <= 4) {
     prm.wct = wb + w.wct;
     if (c->d_max <= 3) build_wct<R, 3><<<c->n_sites, 64, 0, s>>>(prm);
     else build_wct<R, 4><<<c->n_sites, 64, 0, s>>>(prm);
@@ -2072,7 +1923,6 @@ static tq_status values_impl(const tq_chain* c, int batch, const void* theta, in
   prm.c = *c; prm.batch = batch; prm.theta = theta; prm.theta_stride = ts; prm.coef = nullptr; prm.coef_stride = 0;
   prm.env = wb + w.env; prm.epart = wb + w.epart; prm.gpart = nullptr; prm.values = values;
   prm.store_env = 1; prm.mode = 1;
-  prm.use_tc = tc_enabled();
   prm.wct = nullptr; prm.wct_row = 0;
   if (batch == 0) return TQ_OK;
   const int64_t n = (int64_t)batch * c->n_terms;
@@ -2123,8 +1973,8 @@ static tq_status inner_impl(InnerParams& ip, cudaStream_t s) {
     case 8: return launch_inner<R, 8>(ip, s);
     case 16: return launch_inner<R, 16>(ip, s);
     case 32:
-      if (sizeof(R) == 8) return fail(TQ_ERR_UNSUPPORTED, "complex128 mode supports bond dimension <= 16");
-      return launch_inner<R, 32>(ip, s);
+      if constexpr (sizeof(R) == 8) return fail(TQ_ERR_UNSUPPORTED, "complex128 mode supports bond dimension <= 16");
+      else return launch_inner<R, 32>(ip, s);
     default: return fail(TQ_ERR_UNSUPPORTED, "bond dimension exceeds 32");
   }
 }

@@ -45,10 +45,11 @@ def test_mbe_cfg3_bit_exact_cut(golden_large):
     asg = np.array(MC.round_cut(ev), dtype=np.int8)
     np.testing.assert_array_equal(asg, golden_large["cfg3_assignment"])
     assert MC.cut_value(g, asg) == float(golden_large["cfg3_cut"])
-    loss, grad = MC.mbe_objective(c, g)(th)
     ref = float(golden_large["cfg3_loss"])
-    assert abs(loss - ref) < 1e-5 * max(1.0, abs(ref))
-    assert grad_ok64(grad, golden_large["cfg3_grad"])
+    for dtype in ("complex128", "complex64"):   # the drop-in default and the fast path
+        loss, grad = MC.mbe_objective(c, g, dtype=dtype)(th)
+        assert abs(loss - ref) < 1e-5 * max(1.0, abs(ref)), dtype
+        assert grad_ok64(grad, golden_large["cfg3_grad"]), dtype
 
 
 def test_solve_maxcut_small_graphs():

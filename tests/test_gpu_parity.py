@@ -38,7 +38,7 @@ def test_golden_complex64(golden_small):
             continue
         ran += 1
         assert abs(v - case["value"]) <= tol64(case["value"], h), (case["name"], v, case["value"])
-        assert grad_ok64(g, case["grad"]), (case["name"], np.max(np.abs(g - np.array(case["grad"]))))
+        assert grad_ok64(g, case["grad"], h, case["value"]), (case["name"], np.max(np.abs(g - np.array(case["grad"]))))
     assert ran >= 15
 
 
@@ -76,13 +76,13 @@ def test_cfg2_batch256_against_oracle(golden_small):
         case = golden_small["cases"][1 + b]
         np.testing.assert_array_equal(th[b], np.array(case["theta"]))
         assert abs(v[b] - case["value"]) <= tol64(case["value"], h)
-        assert grad_ok64(g[b], case["grad"])
+        assert grad_ok64(g[b], case["grad"], h, case["value"])
     # a few more sets against the oracle restatement
     oc, ot = O.ry_cz_layers(100, 10), O.tfim_terms(100)
     for b in (17, 255):
         ov, og = O.grad_expval_tt(oc, ot, th[b])
         assert abs(v[b] - ov) <= tol64(ov, h)
-        assert grad_ok64(g[b], og)
+        assert grad_ok64(g[b], og, h, ov)
 
 
 def test_deterministic_repeats():
