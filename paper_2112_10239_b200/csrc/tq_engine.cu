@@ -69,6 +69,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
                          // folded cores (A, A2 ping-pong) and P (dense) are cp.async-prefetched
   int32_t a2;            // second folded-core buffer (direct path)
   int32_t wc;            // fused path: per-site channel-pair 2x2 bracket matrices + nonzero mask
+  int32_t lrpf;          // chi >= 16 gradient LR sweep: A (ping-pong A / A2) and P cp.async-prefetched
   int32_t team_bytes;
 };
 
@@ -219,6 +220,16 @@ __device__ __forceinline__ void async_core(C* dst, const C* src, int cl, int cr,
   for (int e = tid; e < 2 * np; e += TEAM) {
     const int sidx = e >= np, r = e - sidx * np;
     async_elem(dst + sidx * MS + (r >> lcr) * LD + (r & (cr - 1)), src + e);
+  }
+}
+// nch stored environments [nch][cr][cr] (dense, HBM) -> padded LD layout in shared memory
+template <typename C, int LD, int TEAM>
+__device__ __forceinline__ void async_env(C* dst, const C* src, int nch, int cr, int lcr, int tid) {
+  constexpr int MS = LD * LD;
+  const int lper = 2 * lcr;
+  for (int e = tid; e < (nch << lper); e += TEAM) {
+    const int ch = e >> lper, r = e & ((1 << lper) - 1);
+    async_elem(dst + ch * MS + (r >> lcr) * LD + (r & (cr - 1)), src + e);
   }
 }
 // n contiguous complex elements (element granularity: offsets are only element-aligned)
@@ -461,6 +472,15 @@ __device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::
   }
 }
 
+__device__ __forceinline__ int tree_index(const int* ocode, int nops, int al, int be) {
+  int idx = 0;
+  for (int oi = 0; oi < nops; ++oi) {
+    const int c = ocode[oi];
+    if (oc_bits(c)) idx |= oc_digit(c, al, be) << oc_toff(c);
+  }
+  return idx;
+}
+
 // Column adjoint on the compact tree: U_last[idx] = sum over passthrough-matched (alpha, beta)
 // of the core cotangent (G[0], G[1])[alpha][beta] (read straight from HBM, dense [2][cl][cr]);
 // walking down, every trainable rotation accumulates Im<U_l, sigma V_l> (per-warp partials in
@@ -478,7 +498,15 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
   const int nlast = 1 << (oc_toff(clast) + oc_bits(clast));
   int npb = 0;
   for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
-  for (int e = tid; e < nlast; e += TEAM) {
+  if (st.pass_count == 0) {
+    // every bond bit is introduced by an op here: (alpha, beta) -> tree index is a bijection
+    // onto the last level, so G is read coalesced in its natural order and scattered in smem
+    for (int pi = tid; pi < np; pi += TEAM) {
+      const int e = tree_index(ocode, nops, pi >> lcr, pi & ((1 << lcr) - 1));
+      ua[2 * e] = gg[pi]; ua[2 * e + 1] = gg[np + pi];
+    }
+  }
+  for (int e = tid; st.pass_count && e < nlast; e += TEAM) {
     int al = 0, be = 0;
     for (int oi = 0; oi < nops; ++oi) {
       const int c = ocode[oi];
@@ -612,6 +640,8 @@ __device__ __forceinline__ void pair_adjoint_warp(int nops, int al, int be, cons
 template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, typename FA, typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
   // CTA: the A operand is stored as X (kk x m) and used as X^H; CTB likewise for B (n x kk).
+  // (chi = 32 on the tensor pipe with 3xTF32 mma.sync was measured and reverted: its biased fp32
+  // accumulation drifts the norm over long chains, profiles/r02_mma3_tf32_trial.txt)
   if (LD >= 17 && n >= 16 && m >= 4) {
     // 4 rows x 2 columns (j, j + n/2) per item: 4 broadcast A loads + 2 B loads per 8 cMAC
     const int hn = n >> 1;
@@ -1146,6 +1176,10 @@ lr_sweep(Params p) {
   // cp.async-prefetched one stage ahead (A(q+1) during site q's Lambda GEMM, P(q+1) after
   // site q's G), so the sweep never waits on HBM/L2 at a site boundary.
   const bool pf = MODE == 0 && FUSE && p.L.direct;
+  // chi >= 16 gradient sweep: the same one-stage-ahead prefetch in the padded layout.  Group order
+  // per site: A(q+1) at the site's start, then blob(q+2) and P(q+1) at its end, so "all but the
+  // newest group" at a site's start is A(q) + its blob, and P(q) is waited only before the G GEMM.
+  const bool pf2 = MODE == 0 && !FUSE && CHI >= 16 && p.L.lrpf;
   C* const abuf1 = reinterpret_cast<C*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.a2);
   blob_prefetch(raw0, blob + p.c.blob_off[seg.site_begin], p.c.blob_max, tid, TEAM);
   blob_wait();
@@ -1161,9 +1195,17 @@ lr_sweep(Params p) {
       async_core<C, LD, TEAM>(sm.A, env_g + s0.a_off, s0.chi_l, s0.chi_r, 31 - __clz(s0.chi_r), tid);
       async_commit();
     }
+    if (pf2) {
+      async_core<C, LD, TEAM>(sm.A, env_g + s0.a_off, s0.chi_l, s0.chi_r, 31 - __clz(s0.chi_r), tid);
+      async_commit();
+    }
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM, !pf);
     if (pf) {
       async_dense<C, TEAM>(PIN, env_g + s0.env_in, s0.rl_db * s0.chi_r * s0.chi_r, tid);
+      async_commit();
+    }
+    if (pf2) {
+      async_env<C, LD, TEAM>(PIN, env_g + s0.env_in, s0.rl_db, s0.chi_r, 31 - __clz(s0.chi_r), tid);
       async_commit();
     }
   }
@@ -1179,8 +1221,8 @@ lr_sweep(Params p) {
     const int npin = MODE == 0 ? st.rl_db : 1;
     R th_pre = R(0);      // next site's first angle, requested ahead of the Lambda GEMM
     bool wct_as = false;  // next site's bracket-matrix row already on its way (cp.async)
-    C* const Acur = (pf && (q & 1)) ? abuf1 : sm.A;
-    if (pf) {
+    C* const Acur = ((pf || pf2) && (q & 1)) ? abuf1 : sm.A;
+    if (pf || pf2) {
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // A(q) landed (P(q) may still be in flight)
     } else {
       // stored right environments at cut k+1 -> PIN (dense cr x cr in HBM), folded core -> A
@@ -1198,6 +1240,11 @@ lr_sweep(Params p) {
       }
     }
     team_sync<TEAM>();
+    if (pf2 && has_next) {   // A(q+1) into the other buffer; lands during this site's GEMMs
+      const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+      async_core<C, LD, TEAM>((q & 1) ? sm.A : abuf1, env_g + sn.a_off, sn.chi_l, sn.chi_r, 31 - __clz(sn.chi_r), tid);
+      async_commit();
+    }
     STAGE(0);
     STAGE(1);
     if constexpr (FUSE && MODE == 0) {
@@ -1224,13 +1271,13 @@ lr_sweep(Params p) {
       // M[a][s] = Lam[a] * A[s]
       gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cl, 1,
           [&](int t, int) { return LAM + (t >> 1) * MS; },
-          [&](int t, int) { return sm.A + (t & 1) * MS; },
+          [&](int t, int) { return Acur + (t & 1) * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
       if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM>(tid, da, db, M, WC, sm.BR, lcl, lcr);
       else bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
-      blob_wait();
+      if (!pf2) blob_wait();   // pf2: the blob landed with A(q) at the site's start
       team_sync<TEAM>();
       STAGE(3);
     }
@@ -1249,6 +1296,10 @@ lr_sweep(Params p) {
       sm.sel(cur);
     }
     if constexpr (MODE == 0) {
+      if (pf2) {   // P(q) (and A(q+1)) landed
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        team_sync<TEAM>();
+      }
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
       if (!(FUSE && p.L.direct)) gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
           [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
@@ -1342,6 +1393,11 @@ lr_sweep(Params p) {
       async_dense<C, TEAM>(PIN, env_g + sn.env_in, sn.rl_db * sn.chi_r * sn.chi_r, tid);
       async_commit();
     }
+    if (pf2 && has_next) {   // P(q+1): PIN is no longer read (the barrier after the G GEMM)
+      const tq_site sn = *reinterpret_cast<const tq_site*>(sm.sel_sbuf(cur ^ 1) + 1);
+      async_env<C, LD, TEAM>(PIN, env_g + sn.env_in, sn.rl_db, sn.chi_r, 31 - __clz(sn.chi_r), tid);
+      async_commit();
+    }
   }
   STAGE_END(1);
 }
@@ -1391,6 +1447,17 @@ adj_sweep(Params p, AdjLayout A) {
   int4* raw = reinterpret_cast<int4*>(base + A.raw);
   const int4* blob = reinterpret_cast<const int4*>(p.c.blob) + p.c.blob_off[si];
   blob_prefetch(raw, blob, p.c.blob_max, tid, TEAM);   // every 16-byte unit in flight at once
+  if (CHI >= 16 && A.tree) {
+    // the core cotangent (written by lr_sweep, long evicted from L2) is read after the forward
+    // tree: pull its lines into L2 now so that read costs an L2 hit, not an HBM round trip
+    const tq_site* sg = p.c.sites + si;
+    const int64_t goff = sg->g_off;
+    const tq_segment* sgs = p.c.segs + reinterpret_cast<const int*>(blob)[3];
+    const char* gl = reinterpret_cast<const char*>(reinterpret_cast<const C*>(p.env) + (size_t)b * p.c.env_total +
+                                                    sgs->env_base + goff);
+    const int nbytes = 2 * sg->chi_l * sg->chi_r * (int)sizeof(C);
+    for (int o = tid * 128; o < nbytes; o += TEAM * 128) asm volatile("prefetch.global.L2 [%0];" :: "l"(gl + o));
+  }
   blob_wait();
   team_sync<TEAM>();
   const tq_site st = *reinterpret_cast<const tq_site*>(raw + 1);
@@ -1688,8 +1755,9 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.br = (int32_t)off; off += (size_t)2 * D * ms;
   L.pin = (int32_t)off;
   if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
+  L.lrpf = (lr && mode == 0 && chi >= 16) ? 1 : 0;
   L.a2 = (int32_t)off;
-  if (L.direct) off += 2 * ms;
+  if (L.direct || L.lrpf) off += 2 * ms;
   off = align_up(off, 16);
   L.wc = (int32_t)off;
   if (fused || wbr) { const int dm = D <= 3 ? 3 : 4; off += align_up((size_t)dm * dm * 4 * csz + 16, 16); }
