@@ -69,6 +69,31 @@ tq_status tq_tt_values(int n_qubits, int dtype, int batch, int chi_cap, const vo
                        int n_terms, void* values, double* norm2, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* Straight-through gradient of a truncated run (reference grad_expval with eps > 0 or a binding
+ * chi_max: _tt_taped_state autodiff.py:339-363, _tt_taped_split autodiff.py:315-336).  The taped
+ * state is built without centre moves; each two-site split keeps its SVD factor U_k (m <= n) or
+ * Vh_k as a constant and the other factor as the differentiable projection.
+ *   tq_tt_taped   runs that construction for B theta-sets, writes the per-term values of the
+ *                 final train (an empty term gives <psi|psi>, as the tape) and records every
+ *                 split's constant factor + (k, side, rescale) into `tape`
+ *                 (tq_tt_tape_bytes(n_two_site, B, cap, dtype) bytes);
+ *   tq_tt_replay  re-runs it for `rows` angle sets with the constants of the recorded theta-set
+ *                 parent[row] frozen (no SVD).  With the constants frozen each angle enters as
+ *                 c + a cos(t/2) + b sin(t/2), so the shift rule on replayed values is the exact
+ *                 straight-through derivative.
+ * n_two_site = number of kind-2 rows of the gate table (the tape slots per theta-set). */
+size_t tq_tt_tape_bytes(int n_two_site, int batch, int chi_cap, int dtype);
+tq_status tq_tt_taped(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int batch,
+                      const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
+                      const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
+                      int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags, void* tape,
+                      void* workspace, size_t workspace_bytes, void* stream);
+tq_status tq_tt_replay(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int rows,
+                       const void* theta, int64_t theta_stride, int chi_cap, const int32_t* parent, int tape_batch,
+                       const void* tape, const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
+                       const int8_t* codes, int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* Measured FP64 FMA throughput of this GPU (the roofline denominator of the complex128 path). */
 tq_status tq_tt_dfma_peak(int32_t iters, void* stream, double* tflops_out);
 

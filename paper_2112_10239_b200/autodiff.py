@@ -115,6 +115,25 @@ def _truncated_expval(circuit, ham, arr, eps, chi_max, dtype, device):
     return e.real
 
 
+def _straight_through(circuit, ham, arr, eps, chi_max, dtype, device):
+    """(E [B], grad [B, P]) of the reference's taped truncated evaluation (truncated.straight_through);
+    the taped value gets the same residue and finiteness checks as every energy."""
+    from . import truncated as TR
+
+    terms = _terms(ham, circuit.n_qubits)
+    vals, grad = TR.straight_through(circuit, terms, arr, eps, chi_max, dtype=dtype, device=device)
+    e = vals @ np.array([c for c, _ in terms], dtype=complex) if terms else np.zeros(arr.shape[0], complex)
+    if not (np.all(np.isfinite(e)) and np.all(np.isfinite(grad))):
+        from .errors import NotFinite
+        raise NotFinite("engine produced NaN or Inf")
+    tol = E.residue_tol(dtype, sum(abs(c) for c, _ in terms))
+    worst = float(np.max(np.abs(e.imag))) if e.size else 0.0
+    if worst > tol:
+        from .errors import NonHermitianResidue
+        raise NonHermitianResidue(f"imaginary residue {worst:.3e} exceeds {tol:.0e}")
+    return e.real, grad
+
+
 def _device(device):
     if device is None:
         if not torch.cuda.is_available():
@@ -162,8 +181,11 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
     eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, single = _check_theta(circuit, theta)
     if _truncating(circuit, eps, chi_max):
-        raise InputError("gradients through a truncated split are not supported (the reference's are "
-                         "straight-through, autodiff.py:10-13); use eps=0 and chi_max >= the exact bond")
+        # the reference's straight-through gradient of its taped truncated state (autodiff.py:10-13,
+        # 315-363): value of the taped construction and the gradient with the split constants frozen
+        v, g = _straight_through(circuit, ham, arr, eps, chi_max, dtype if dtype != "complex64" else "complex128",
+                                 device)
+        return (float(v[0]), g[0]) if single else (v, g)
     dev = _device(device)
     terms = _terms(ham, circuit.n_qubits)
     dp = E.device_plan(circuit, terms, "energy", arr.shape[0], dev, segments, dtype=dtype)

@@ -8,13 +8,13 @@ Mirrors ``tnsim.cli`` (``cli.py:70-160,238-248,274-332``):
   numerical errors.
 
 Differences:
-- ``--engine`` takes ``b200`` (default; ``tt`` is an alias) and the reference's ``dense``, which
-  keeps its meaning: exact values, ``--eps``/``--chi`` ignored, at most 26 qubits; the values
-  come from the B200 engine's exact path.
+- ``--engine`` takes the reference's choices with the reference's default: ``dense`` (exact
+  values, ``--eps``/``--chi`` ignored, at most 26 qubits) and ``tt`` (``b200`` is an alias).
+  Both run on the B200 engines; ``dense`` is their exact path.
 - ``--eps`` / ``--chi`` select the truncated TT engine (row f3) whenever they can truncate.
-  ``grad --method ad`` then raises an input error: the reference's gradient through a
-  truncated split is straight-through (autodiff.py:10-13).  ``shift`` and ``fd`` work as in
-  the reference, on truncated forwards.
+  ``grad --method ad`` then returns the reference's straight-through gradient of its taped
+  truncated state (autodiff.py:10-13,315-363; truncated.straight_through); ``shift`` and ``fd``
+  work as in the reference, on truncated forwards.
 - ``ptrace`` and ``paths`` (density matrices, contraction-order search) are outside the hot
   path and are not offered.
 - ``--dtype`` picks complex128 (default, the reference's precision) or complex64.
@@ -199,7 +199,7 @@ def _common(sp) -> None:
 
 
 def _engine(sp) -> None:
-    sp.add_argument("--engine", choices=("b200", "tt", "dense"), default="b200")
+    sp.add_argument("--engine", choices=("dense", "tt", "b200"), default="dense")
     sp.add_argument("--chi", type=int, default=None, help="TT bond cap (truncated engine when it binds)")
     sp.add_argument("--eps", type=float, default=0.0, help="TT relative truncation threshold")
 

@@ -86,7 +86,16 @@ struct Params {
   void* cores;     // [B][n][2 cap^2] complex
   void* envl;      // [B][n+1][cap^2]
   void* envr;      // [B][n+1][cap^2]
+  // straight-through tape (PH_TAPE writes it, PH_REPLAY reads it): per recorded theta-set and
+  // two-site gate, the split's constant isometric factor (U_k, m x k, or Vh_k, k x n) in a slot
+  // of 2 cap^2 complex, and its (k, side, rescale)
+  void* tape;
+  struct TapeMeta* meta;
+  const int32_t* parent;   // PH_REPLAY: the recorded theta-set whose tape row b replays
+  int32_t n2;              // two-site gates in the program (tape slots per theta-set)
 };
+
+struct TapeMeta { int32_t k; int32_t left_iso; double scale; };
 
 // Shared scratch of one CTA: X and V are (2cap) x (2cap) complex, column-major with leading
 // dimension 2cap (Jacobi columns are contiguous, rows are spread over lanes).
@@ -574,6 +583,73 @@ __device__ void two_site(Scratch<R, CAP>& s, const Params& p, typename CT<R>::T*
   __syncthreads();
 }
 
+// Straight-through split replay (reference _tt_taped_split, autodiff.py:315-336): the merged,
+// gated block M (m x n) is split with the RECORDED constant factor of the unshifted run instead
+// of a fresh SVD -- left = U_k, right = rescale U_k^H M when m <= n; right = Vh_k,
+// left = rescale M Vh_k^H otherwise.  The tape's value as a function of one angle (constants
+// frozen) is a trigonometric polynomial, so shifted replays give its exact derivative.
+template <typename R, int CAP>
+__device__ void replay_two_site(Scratch<R, CAP>& s, typename CT<R>::T* cores, int32_t* dims, int i,
+                                const typename CT<R>::T* iso, TapeMeta mt) {
+  using C = typename CT<R>::T;
+  constexpr int SLOT = 2 * CAP * CAP;
+  const int tid = threadIdx.x;
+  const int cl = dims[i], cm = dims[i + 1], cr = dims[i + 2];
+  C* A = cores + (size_t)i * SLOT;
+  C* B = cores + (size_t)(i + 1) * SLOT;
+  const int m = 2 * cl, n = 2 * cr, k = mt.k;
+  const R sc = R(mt.scale);
+  C* As = s.V;
+  C* Bs = s.V + SLOT;
+  C* M = s.X;                                     // row-major m x n
+  for (int e = tid; e < cl * 2 * cm; e += NT) As[e] = A[e];
+  for (int e = tid; e < cm * 2 * cr; e += NT) Bs[e] = B[e];
+  __syncthreads();
+  for (int e = tid; e < cl * cr; e += NT) {
+    const int a = e / cr, b = e - a * cr;
+    C t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = cmk<C>(R(0), R(0));
+    for (int mid = 0; mid < cm; ++mid) {
+      const C a0 = As[(a * 2 + 0) * cm + mid], a1 = As[(a * 2 + 1) * cm + mid];
+      const C b0 = Bs[(mid * 2 + 0) * cr + b], b1 = Bs[(mid * 2 + 1) * cr + b];
+      cfma(t[0], a0, b0); cfma(t[1], a0, b1); cfma(t[2], a1, b0); cfma(t[3], a1, b1);
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      C acc = cmk<C>(R(0), R(0));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cfma(acc, s.G[o * 4 + q], t[q]);
+      M[(a * 2 + (o >> 1)) * n + (o & 1) * cr + b] = acc;
+    }
+  }
+  __syncthreads();
+  if (mt.left_iso) {
+    for (int e = tid; e < m * k; e += NT) A[e] = iso[e];
+    for (int e = tid; e < k * n; e += NT) {
+      const int rr = e / n, col = e - rr * n;
+      C acc = cmk<C>(R(0), R(0));
+      for (int row = 0; row < m; ++row) cfmac(acc, iso[row * k + rr], M[row * n + col]);
+      B[e] = cmk<C>(acc.x * sc, acc.y * sc);
+    }
+  } else {
+    for (int e = tid; e < k * n; e += NT) B[e] = iso[e];
+    for (int e = tid; e < m * k; e += NT) {
+      const int row = e / k, rr = e - row * k;
+      C acc = cmk<C>(R(0), R(0));
+      for (int col = 0; col < n; ++col) {   // acc += M[row][col] conj(Vh[rr][col])
+        const C x = M[row * n + col], v = iso[rr * n + col];
+        acc.x = fma(x.x, v.x, fma(x.y, v.y, acc.x));
+        acc.y = fma(x.y, v.x, fma(-x.x, v.y, acc.y));
+      }
+      A[e] = cmk<C>(acc.x * sc, acc.y * sc);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) dims[i + 1] = k;
+  __syncthreads();
+}
+
 // ---- environments and term windows ---------------------------------------------------------
 // x' [c][d] = sum_{a,s,s'} conj(A[a][s][c]) P[s][s'] x[a][b] A[b][s'][d]   (P = I for code 0)
 template <typename R, int CAP>
@@ -636,6 +712,11 @@ __device__ void right_step(Scratch<R, CAP>& s, const typename CT<R>::T* A, int c
 }
 
 constexpr int PH_RUN = 1, PH_COMPRESS = 2, PH_VALUES = 4;
+// straight-through gradient: PH_TAPE runs the reference's TAPED state construction
+// (_tt_taped_state, autodiff.py:339-363: no centre moves, every two-site gate split as in
+// _tt_taped_split) and records each split's constant factor; PH_REPLAY re-runs it at shifted
+// angles with those factors frozen
+constexpr int PH_TAPE = 8, PH_REPLAY = 16;
 
 template <typename R, int CAP, int PHASE>
 __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
@@ -663,6 +744,9 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
   __syncthreads();
   int center = 0;
   double disc = 0.0;
+  constexpr bool TAPED = (PHASE & (PH_TAPE | PH_REPLAY)) != 0;
+  constexpr int TSLOT = 2 * CAP * CAP;
+  int j2 = 0;   // two-site gates so far (tape slot)
   for (int gi = 0; gi < p.n_gates; ++gi) {
     const tq_tgate& g = p.gates[gi];
     if (tid == 0) gate_matrix<R>(g, theta_b, s.G);
@@ -682,13 +766,32 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
       __syncthreads();
       continue;
     }
+    if constexpr (TAPED) {
+      if constexpr ((PHASE & PH_REPLAY) != 0) {
+        const size_t slot = (size_t)p.parent[b] * p.n2 + j2;
+        replay_two_site<R, CAP>(s, cores, dims, site, reinterpret_cast<const C*>(p.tape) + slot * TSLOT, p.meta[slot]);
+      } else {
+        const int m = 2 * dims[site], nn = 2 * dims[site + 2];
+        two_site<R, CAP>(s, p, cores, dims, site, disc, flag);
+        const size_t slot = (size_t)b * p.n2 + j2;
+        const int k = dims[site + 1];
+        C* dst = reinterpret_cast<C*>(p.tape) + slot * TSLOT;
+        const C* src = cores + (size_t)(m <= nn ? site : site + 1) * SLOT;   // the constant factor
+        const int cnt = m <= nn ? m * k : k * nn;
+        for (int e = tid; e < cnt; e += NT) dst[e] = src[e];
+        if (tid == 0) { p.meta[slot].k = k; p.meta[slot].left_iso = m <= nn; p.meta[slot].scale = double(s.scale); }
+        __syncthreads();
+      }
+      ++j2;
+      continue;
+    }
     while (center < site) { shift_right<R, CAP>(s, cores, dims, center, flag); ++center; }
     while (center > site) { shift_left<R, CAP>(s, cores, dims, center, flag); --center; }
     const int m = 2 * dims[site], nn = 2 * dims[site + 2];
     two_site<R, CAP>(s, p, cores, dims, site, disc, flag);
     center = m <= nn ? site + 1 : site;
   }
-  if (tid == 0) { p.discarded[b] = disc; if (p.centers) p.centers[b] = center; }
+  if (tid == 0) { if (p.discarded) p.discarded[b] = disc; if (p.centers) p.centers[b] = center; }
   __syncthreads();
   }
   if constexpr ((PHASE & PH_COMPRESS) != 0) {
@@ -716,8 +819,12 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
   C* xb = s.V + ESLOT;
   for (int t = 0; t < p.n_terms; ++t) {
     const int lo = p.term_lo[t], hi = p.term_hi[t];
-    if (hi < lo) {
-      if (tid == 0) p.values[(size_t)b * p.n_terms + t] = make_double2(1.0, 0.0);
+    if (hi < lo) {   // an empty term: 1 (untaped expval), <psi|psi> on the tape (_tt_term_nodes)
+      if (tid == 0) {
+        const C nrm = envl[(size_t)n * ESLOT];
+        p.values[(size_t)b * p.n_terms + t] =
+            (PHASE & (PH_TAPE | PH_REPLAY)) ? make_double2(double(nrm.x), double(nrm.y)) : make_double2(1.0, 0.0);
+      }
       continue;
     }
     const int c0 = dims[lo];
@@ -934,6 +1041,68 @@ tq_status tq_tt_compress(int n_qubits, int dtype, int batch, double eps, int chi
   p.n = n_qubits; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max; p.eps = eps;
   p.discarded = discarded; p.bonds = bonds; p.flags = flags; p.centers = centers; p.cores = cores;
   return dispatch<PH_COMPRESS>(p, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t tq_tt_tape_bytes(int n_two_site, int batch, int chi_cap, int dtype) {
+  if (n_two_site < 0 || batch < 1 || chi_cap < 1) return 0;
+  const size_t csz = dtype == TQ_C128 ? 16 : 8;
+  const int c = tqt::cap_bucket(chi_cap);
+  const size_t slots = (size_t)batch * (n_two_site > 0 ? n_two_site : 1);
+  return tqt::align256(slots * 2 * c * c * csz) + slots * sizeof(tqt::TapeMeta);
+}
+
+static tq_status tt_taped_common(int phase, int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype,
+                                 int batch, const void* theta, int64_t theta_stride, double eps, int chi_cap,
+                                 int chi_max, const int32_t* parent, const int32_t* term_lo, const int32_t* term_hi,
+                                 const int32_t* code_off, const int8_t* codes, int n_terms, void* values,
+                                 double* norm2, int32_t* bonds, int32_t* flags, void* tape, int tape_batch,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_taped", n_qubits, batch, chi_cap, dtype) || n_gates < 0 || n_terms < 0 || n_two_site < 0)
+    return TQ_ERR_INPUT;
+  const WsParts w = ws_parts(n_qubits, batch, chi_cap, dtype);
+  if (workspace_bytes < w.total) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "tq_tt_taped: workspace %zu < %zu bytes", workspace_bytes, w.total);
+    return TQ_ERR_WORKSPACE;
+  }
+  Params p{};
+  p.n = n_qubits; p.n_gates = n_gates; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max;
+  p.n_terms = n_terms; p.gates = reinterpret_cast<const tq_tgate*>(gates); p.theta = theta;
+  p.theta_stride = theta_stride; p.eps = eps; p.term_lo = term_lo; p.term_hi = term_hi;
+  p.code_off = code_off; p.codes = codes; p.values = reinterpret_cast<double2*>(values);
+  p.discarded = nullptr; p.norm2 = norm2; p.bonds = bonds; p.flags = flags;
+  unsigned char* base = reinterpret_cast<unsigned char*>(workspace);
+  p.cores = base + w.cores; p.envl = base + w.envl; p.envr = base + w.envr;
+  const size_t csz = dtype == TQ_C128 ? 16 : 8;
+  const int c = cap_bucket(chi_cap);
+  const size_t slots = (size_t)tape_batch * (n_two_site > 0 ? n_two_site : 1);
+  p.tape = tape;
+  p.meta = reinterpret_cast<TapeMeta*>(reinterpret_cast<unsigned char*>(tape) + align256(slots * 2 * c * c * csz));
+  p.parent = parent; p.n2 = n_two_site;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
+  return phase == PH_TAPE ? dispatch<PH_RUN | PH_TAPE | PH_VALUES>(p, dtype, st)
+                          : dispatch<PH_RUN | PH_REPLAY | PH_VALUES>(p, dtype, st);
+}
+
+tq_status tq_tt_taped(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int batch,
+                      const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
+                      const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
+                      int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags, void* tape,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  return tt_taped_common(tqt::PH_TAPE, n_qubits, gates, n_gates, n_two_site, dtype, batch, theta, theta_stride, eps,
+                         chi_cap, chi_max, nullptr, term_lo, term_hi, code_off, codes, n_terms, values, norm2, bonds,
+                         flags, tape, batch, workspace, workspace_bytes, stream);
+}
+
+tq_status tq_tt_replay(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int rows,
+                       const void* theta, int64_t theta_stride, int chi_cap, const int32_t* parent, int tape_batch,
+                       const void* tape, const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
+                       const int8_t* codes, int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  return tt_taped_common(tqt::PH_REPLAY, n_qubits, gates, n_gates, n_two_site, dtype, rows, theta, theta_stride, 0.0,
+                         chi_cap, -1, parent, term_lo, term_hi, code_off, codes, n_terms, values, norm2, bonds, flags,
+                         const_cast<void*>(tape), tape_batch, workspace, workspace_bytes, stream);
 }
 
 size_t tq_tt_values_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype) {

@@ -122,10 +122,10 @@ def bench_tfim(n_qubits: int = 500, n_gates: int = 5000, chi_max: int | None = 1
     The forward phase runs the truncated TT engine (row f3, ``truncated.py``), which repeats
     the reference's simulate_tt with (eps, chi_max).  ``expval``, ``max_bond``,
     ``bond_histogram`` and ``discarded_weight`` therefore follow the reference's semantics.
-    The gradient phase runs the exact engine.  It is offered only when (eps, chi_max)
-    truncate nothing: the reference's gradient through a truncated split is straight-through
-    and documented as best-effort (autodiff.py:10-13), so a truncating ``--grad`` run raises
-    ``InputError``."""
+    The gradient phase is ``grad_expval(eps, chi_max)`` as in the reference: the exact engine
+    when (eps, chi_max) truncate nothing, else the reference's straight-through gradient of its
+    taped truncated state (``truncated.straight_through``, autodiff.py:10-13,315-363), whose
+    ``grad_value`` is the taped construction's energy."""
     from . import autodiff as AD
     from . import chain as C
     from . import truncated as TR
@@ -138,10 +138,6 @@ def bench_tfim(n_qubits: int = 500, n_gates: int = 5000, chi_max: int | None = 1
         return circuit, tfim(n_qubits, j, h), AD.init_params(circuit.n_params, generator(seed))
 
     (circuit, ham, theta), wall["build"], _ = measure(build)
-    truncating = AD._truncating(circuit, eps, chi_max)
-    if grad and truncating:
-        raise InputError("a gradient through a truncated split is not supported; rerun with --no-grad "
-                         "(or eps=0 and chi_max >= the exact bond)")
     terms = C.normalize_terms(ham)
 
     def forward():
@@ -156,7 +152,8 @@ def bench_tfim(n_qubits: int = 500, n_gates: int = 5000, chi_max: int | None = 1
                "bond_histogram": {str(k): int(v) for k, v in sorted(hist.items())},
                "discarded_weight": float(res.discarded[0])}
     if grad:
-        (gval, gvec), wall["gradient"], pk = measure(lambda: AD.grad_expval(circuit, ham, theta, dtype=dtype))
+        (gval, gvec), wall["gradient"], pk = measure(lambda: AD.grad_expval(circuit, ham, theta, eps=eps,
+                                                                            chi_max=chi_max, dtype=dtype))
         peak = max(peak, pk)
         outputs["grad_value"] = float(gval)
         outputs["grad_norm"] = float(np.linalg.norm(gvec))

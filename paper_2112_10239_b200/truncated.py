@@ -10,9 +10,9 @@ Semantics follow the reference ``simulate_tt`` / ``apply_gate_tt`` (``tt.py:85-2
   the retained weight, and puts sigma on the thin side;
 - the discarded weight accumulates per theta-set.
 
-This engine is forward-only.  The reference's gradient through a truncated split is
-straight-through and documented as best-effort (``autodiff.py:10-13``), so gradients stay
-on the exact engine.
+Gradients through truncated splits follow the reference's straight-through tape
+(``autodiff.py:10-13,315-363``): :func:`straight_through` records the taped construction's
+constant SVD factors and differentiates the frozen-constant value exactly by batched replays.
 """
 
 from __future__ import annotations
@@ -399,3 +399,112 @@ def compress(train: GPUTrain, eps: float, chi_max=None) -> GPUTrain:
                                   -1 if chi_max is None else int(chi_max), out.cores.data_ptr(), out.bonds.data_ptr(),
                                   out.centers.data_ptr(), out.discarded.data_ptr(), out.flags.data_ptr(), _stream()))
     return out.check()
+
+
+# ----------------------------------------------------------------------------- straight-through gradient
+def _check_flags(flags, cap):
+    f = flags.cpu().numpy()
+    if np.any(f == 2):
+        from .errors import NotFinite
+        raise NotFinite("truncated engine produced NaN")
+    if np.any(f):
+        raise BondTooLarge(f"a bond exceeded the truncated engine's capacity chi={cap}; pass chi_max <= {cap}")
+
+
+def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=None, *, dtype: str = "complex128",
+                     device=None, want_grad: bool = True, rows_per_launch: int | None = None):
+    """The reference's gradient through truncated splits (``grad_expval`` with eps > 0 or a binding
+    chi_max, autodiff.py:315-363,471-487): value and straight-through gradient for every theta-set.
+
+    1. ``tq_tt_taped`` builds the TAPED state of each theta-set (no centre moves; every two-site
+       split keeps U_k, or Vh_k, as a constant and the other factor as the differentiable
+       projection) and records those constants;
+    2. ``tq_tt_replay`` re-runs the construction for every shifted angle set with the constants of
+       its theta-set frozen.  Frozen, each gate enters linearly and each angle as
+       c + a cos(t/2) + b sin(t/2), so the reference's reverse-mode result equals the exact shift
+       rule on the replayed values: (E(t + pi/2) - E(t - pi/2)) / 2, and crz's four-term rule
+       (autodiff.py:509-550).  Shifted rows are batched over the SMs, one CTA per row.
+
+    Returns (values [B, T] complex128 of the taped state, grad [B, P] float64 of
+    E = Re sum_t c_t v_t) -- the gradient needs the coefficients, so ``terms`` carry them."""
+    import torch
+
+    from . import _lib
+    from .autodiff import _CRZ_Y1, _CRZ_Y2, _device
+    from .engine import _stream
+
+    cap = check_truncation_args(eps, chi_max)
+    theta = np.atleast_2d(np.asarray(theta, dtype=float))
+    if theta.shape[1] != circuit.n_params:
+        from .errors import ParamCountMismatch
+        raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
+    B, n, P = theta.shape[0], circuit.n_qubits, circuit.n_params
+    dev = _device(device)
+    table, d_gates = _device_gates(circuit, dev)
+    n2 = int(np.sum(table["kind"] == 2))
+    d_lo, d_hi, d_offs, d_codes = _device_terms(terms, n, dev)
+    code = _lib.TQ_C128 if dtype == "complex128" else _lib.TQ_C64
+    tdt = torch.float64 if dtype == "complex128" else torch.float32
+    lib = _lib.load()
+    T = len(terms)
+    coef = np.array([c for c, _ in terms], dtype=complex)
+    tape = torch.empty(int(lib.tq_tt_tape_bytes(n2, B, cap, code)), dtype=torch.uint8, device=dev)
+
+    def run(rows_theta, parent=None):
+        R_ = rows_theta.shape[0]
+        th = torch.tensor(rows_theta, dtype=tdt, device=dev)
+        values = torch.zeros(R_, max(T, 1), 2, dtype=torch.float64, device=dev)
+        norm2 = torch.zeros(R_, dtype=torch.float64, device=dev)
+        bonds = torch.zeros(R_, n + 1, dtype=torch.int32, device=dev)
+        flags = torch.zeros(R_, dtype=torch.int32, device=dev)
+        wsb = int(lib.tq_tt_workspace_bytes(n, R_, cap, code))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        if parent is None:
+            st = lib.tq_tt_taped(n, d_gates.data_ptr(), len(table), n2, code, R_, th.data_ptr(), th.stride(0),
+                                 ctypes.c_double(eps), cap, -1 if chi_max is None else int(chi_max),
+                                 d_lo.data_ptr(), d_hi.data_ptr(), d_offs.data_ptr(), d_codes.data_ptr(), T,
+                                 values.data_ptr(), norm2.data_ptr(), bonds.data_ptr(), flags.data_ptr(),
+                                 tape.data_ptr(), ws.data_ptr(), ctypes.c_size_t(wsb), _stream())
+        else:
+            par = torch.tensor(parent, dtype=torch.int32, device=dev)
+            st = lib.tq_tt_replay(n, d_gates.data_ptr(), len(table), n2, code, R_, th.data_ptr(), th.stride(0), cap,
+                                  par.data_ptr(), B, tape.data_ptr(), d_lo.data_ptr(), d_hi.data_ptr(),
+                                  d_offs.data_ptr(), d_codes.data_ptr(), T, values.data_ptr(), norm2.data_ptr(),
+                                  bonds.data_ptr(), flags.data_ptr(), ws.data_ptr(), ctypes.c_size_t(wsb), _stream())
+        _lib.check(st)
+        _check_flags(flags, cap)
+        return torch.view_as_complex(values).cpu().numpy()[:, :T]
+
+    vals = run(theta)
+    if not want_grad:
+        return vals, None
+    names = [circuit.gates[g].name for g in circuit.trainable]
+    rows, plan = [], []
+    for b in range(B):
+        for k in range(P):
+            shifts = (np.pi / 2, -np.pi / 2, 3 * np.pi / 2, -3 * np.pi / 2) if names[k] == "crz" else (np.pi / 2, -np.pi / 2)
+            idx = []
+            for d in shifts:
+                t = theta[b].copy()
+                t[k] += d
+                idx.append(len(rows))
+                rows.append((b, t))
+            plan.append((b, k, idx))
+    grad = np.zeros((B, P))
+    if not rows:
+        return vals, grad
+    if rows_per_launch is None:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        per_row = int(lib.tq_tt_workspace_bytes(n, 1, cap, code))
+        rows_per_launch = int(max(sms, min(8 * sms, (2 << 30) // max(per_row, 1))))
+    e = np.zeros(len(rows))
+    for c0 in range(0, len(rows), rows_per_launch):
+        chunk = rows[c0:c0 + rows_per_launch]
+        v = run(np.stack([t for _, t in chunk]), [b for b, _ in chunk])
+        e[c0:c0 + len(chunk)] = (v @ coef).real
+    for b, k, idx in plan:
+        if names[k] == "crz":
+            grad[b, k] = _CRZ_Y1 * (e[idx[0]] - e[idx[1]]) - _CRZ_Y2 * (e[idx[2]] - e[idx[3]])
+        else:
+            grad[b, k] = 0.5 * (e[idx[0]] - e[idx[1]])
+    return vals, grad

@@ -92,8 +92,8 @@ def test_exit_codes_without_engine(tmp_path, capsys, monkeypatch, golden_cli):
     assert _run(["expval", "--circuit", str(tmp_path / "bad.json"), "--ham", z], capsys)[0] == 2
     assert _run(["expval", "--circuit", b], capsys)[0] == 2          # --ham is required
     assert _run(["ptrace", "--n", "4"], capsys)[0] == 2               # outside the hot path
-    assert _run(["expval", "--circuit", b, "--ham", z, "--eps", "-1"], capsys)[0] == 2
-    assert _run(["expval", "--circuit", b, "--ham", z, "--chi", "0"], capsys)[0] == 2
+    assert _run(["expval", "--circuit", b, "--ham", z, "--engine", "tt", "--eps", "-1"], capsys)[0] == 2
+    assert _run(["expval", "--circuit", b, "--ham", z, "--engine", "tt", "--chi", "0"], capsys)[0] == 2
     assert _run(["expval", "--circuit", b, "--ham", z, "--engine", "mps"], capsys)[0] == 2
     code, out, _ = _run(["--version"], capsys)
     assert code == 0 and out.strip() == cli.__version__

@@ -76,16 +76,17 @@ def test_grad_methods_match_reference_cli(files, capsys, golden_cli):
 
 def test_truncating_runs_match_reference_cli(files, capsys, golden_cli):
     c, h = str(files / "mixed.json"), str(files / "h5.json")
-    rep = _report(["expval", "--circuit", c, "--ham", h, "--chi", "2"], capsys)
+    rep = _report(["expval", "--circuit", c, "--ham", h, "--engine", "tt", "--chi", "2"], capsys)
     assert abs(rep["outputs"]["value"] - _ref(golden_cli, "expval", ("mixed", "h5", "chi2"))["value"]) < 1e-12
-    rep = _report(["grad", "--circuit", c, "--ham", h, "--chi", "2", "--method", "shift"], capsys)
+    rep = _report(["grad", "--circuit", c, "--ham", h, "--engine", "tt", "--chi", "2", "--method", "shift"], capsys)
     ref = _ref(golden_cli, "grad", ("mixed", "h5", "shift", "chi2"))
     np.testing.assert_allclose(rep["outputs"]["gradient"], ref["gradient"], atol=1e-11)
-    code = cli.run_cli(["grad", "--circuit", c, "--ham", h, "--chi", "2"])   # ad through truncation
-    capsys.readouterr()
-    assert code == 2
+    # the reference's default engine is 'dense': --chi is ignored and the gradient is exact
+    rep = _report(["grad", "--circuit", c, "--ham", h, "--chi", "2"], capsys)
+    ref = _ref(golden_cli, "grad", ("mixed", "h5", "ad"))
+    np.testing.assert_allclose(rep["outputs"]["gradient"], ref["gradient"], atol=1e-11)
     for key, extra in ((("mixed", "chi2"), ["--chi", "2"]), (("mixed", "tt"), [])):
-        rep = _report(["simulate", "--circuit", c] + extra, capsys)
+        rep = _report(["simulate", "--circuit", c, "--engine", "tt"] + extra, capsys)
         ref = _ref(golden_cli, "simulate", key)
         assert rep["outputs"]["bond_dims"] == ref["bond_dims"], key
         assert abs(rep["outputs"]["norm"] - ref["norm"]) < 1e-12
@@ -122,10 +123,39 @@ def test_bench_tfim_matches_reference(capsys, golden_cli):
         again = _report(argv, capsys)
         rep.pop("measured"), again.pop("measured")
         assert rep == again
-    with pytest.raises(InputError):
-        bench_tfim(n_qubits=40, n_gates=2000, chi_max=4, grad=True)    # gradient through truncation
 
 
 def test_maxcut_subcommand(files, capsys):
     rep = _report(["maxcut", "--graph", str(files / "tri.txt"), "--restarts", "2", "--max-iters", "40"], capsys)
     assert rep["outputs"]["cut"] == 2.0 and rep["outputs"]["optimal"] == 2.0
+
+
+@pytest.fixture(scope="module")
+def golden_st():
+    with open(os.path.join(HERE, "golden", "golden_st.json")) as f:
+        return json.load(f)
+
+
+def test_straight_through_cli_matches_reference(files, capsys, golden_st):
+    """``grad --engine tt --chi/--eps`` (method ad) and ``bench tfim --grad --chi``: the reference's
+    straight-through gradient of its taped truncated state (autodiff.py:315-363, bench.py:136-141),
+    against the reference CLI's own reports (make_golden_st.py)."""
+    for run in golden_st["cli"]:
+        argv = list(run["argv"])
+        ref = run["report"]["outputs"]
+        if argv[0] == "grad":
+            argv[argv.index("--circuit") + 1] = str(files / "mixed.json")
+            argv[argv.index("--ham") + 1] = str(files / "h5.json")
+            out = _report(argv, capsys)["outputs"]
+            if run["well_posed"]:   # see test_gpu_trunc.test_straight_through_gradient_matches_reference
+                assert abs(out["value"] - ref["value"]) < 1e-10, argv
+                np.testing.assert_allclose(out["gradient"], ref["gradient"], atol=1e-9, err_msg=str(argv))
+        else:
+            out = _report(argv, capsys)["outputs"]
+            for k in ("gate_count", "n_params", "max_bond", "bond_histogram"):
+                assert out[k] == ref[k], (argv, k)
+            assert abs(out["expval"] - ref["expval"]) < 1e-10
+            if run["well_posed"]:
+                assert abs(out["grad_value"] - ref["grad_value"]) < 1e-9, argv
+                assert abs(out["grad_norm"] - ref["grad_norm"]) < 1e-8 * max(1.0, ref["grad_norm"]), argv
+            assert out["grad_finite"] is True
