@@ -9,7 +9,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "tq_engine.cu"), os.path.join(HERE, "csrc", "tq_trunc.cu")]
-HEADERS = [os.path.join(ROOT, "include", "tq_engine.h"), os.path.join(ROOT, "include", "tq_trunc.h")]
+HEADERS = [os.path.join(ROOT, "include", "tq_engine.h"), os.path.join(ROOT, "include", "tq_trunc.h"),
+           os.path.join(HERE, "csrc", "tq_debug.cuh")]
 LIB = os.path.join(HERE, "libtq_engine.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -19,6 +19,7 @@
 // (tt.py:186-244, autodiff.py:315-402, 190-247); see DESIGN.md for the derivation.
 
 #include <cuda_runtime.h>
+#include "tq_debug.cuh"
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -1021,6 +1022,7 @@ rl_sweep(Params p) {
   constexpr int DMW = (FUSE || WBR) ? FDM : 0;    // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
   const int item = blockIdx.x * TEAMS + team;
@@ -1149,6 +1151,7 @@ lr_sweep(Params p) {
   constexpr int DMW = (FUSE || WBR) ? FDM : 0;    // channel-pair bracket matrices staged with the descriptors
   constexpr int FRT = CHI >= 16 ? 2 : 1;          // rows per fused item
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
   const int item = blockIdx.x * TEAMS + team;
@@ -1429,6 +1432,7 @@ adj_sweep(Params p, AdjLayout A) {
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   constexpr int MAXSAVE = 48;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
   const int nsites = p.c.n_sites;
@@ -1609,6 +1613,7 @@ inner_sweep(InnerParams p) {
   constexpr int MS = LD * LD;
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
   const int team = threadIdx.x / TEAM;
   const int tid = threadIdx.x % TEAM;
   const int b = blockIdx.x * TEAMS + team;

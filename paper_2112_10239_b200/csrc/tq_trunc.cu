@@ -17,6 +17,7 @@
 // tests/mirror_trunc.py is the numpy mirror of exactly this algorithm.
 
 #include <cuda_runtime.h>
+#include "tq_debug.cuh"
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -724,6 +725,7 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
   constexpr int SLOT = 2 * CAP * CAP;
   constexpr int ESLOT = CAP * CAP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
   Scratch<R, CAP>& s = *reinterpret_cast<Scratch<R, CAP>*>(smem_raw);
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
