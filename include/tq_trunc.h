@@ -64,6 +64,11 @@ tq_status tq_tt_run(int n_qubits, const void* gates, int n_gates, int dtype, int
                     int32_t* centers, double* discarded, int32_t* flags, void* stream);
 tq_status tq_tt_compress(int n_qubits, int dtype, int batch, double eps, int chi_cap, int chi_max, void* cores,
                          int32_t* bonds, int32_t* centers, double* discarded, int32_t* flags, void* stream);
+/* apply_gate_tt over a whole circuit on trains the caller already holds (tt.py:186-234): every row
+ * continues from its own cores / bonds / centre, discarded weight accumulates. */
+tq_status tq_tt_apply(int n_qubits, const void* gates, int n_gates, int dtype, int batch, const void* theta,
+                      int64_t theta_stride, double eps, int chi_cap, int chi_max, void* cores, int32_t* bonds,
+                      int32_t* centers, double* discarded, int32_t* flags, void* stream);
 tq_status tq_tt_values(int n_qubits, int dtype, int batch, int chi_cap, const void* cores, const int32_t* bonds,
                        const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
                        int n_terms, void* values, double* norm2, void* workspace, size_t workspace_bytes,
@@ -87,12 +92,24 @@ tq_status tq_tt_taped(int n_qubits, const void* gates, int n_gates, int n_two_si
                       const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
                       const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
                       int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags, void* tape,
+                      const void* init_cores, const int32_t* init_bonds,
                       void* workspace, size_t workspace_bytes, void* stream);
 tq_status tq_tt_replay(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int rows,
                        const void* theta, int64_t theta_stride, int chi_cap, const int32_t* parent, int tape_batch,
                        const void* tape, const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
                        const int8_t* codes, int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags,
+                       const void* init_cores, const int32_t* init_bonds,
                        void* workspace, size_t workspace_bytes, void* stream);
+/* init_cores / init_bonds (optional, may be NULL): an input train (reference TTState, tt.py:38-76)
+ * in the slot layout [n][2 cap^2] with bonds [n+1], shared by every row: the circuit then runs on
+ * that state instead of |0...0>.  With eps = 0 and no binding chi_max every split keeps a square
+ * unitary factor, so the replayed shift rule is the EXACT gradient of <state|U^H H U|state>
+ * (autodiff.py:8-13): the differentiable path for arbitrary input trains. */
+
+/* <a_r|b_r> for every row r of two batches of trains (slot layout, bonds [B][n+1]); out [B] complex
+ * (re, im float64), a conjugated: the reference's tt_inner (tt.py:247-255) on arbitrary trains. */
+tq_status tq_tt_inner(int n_qubits, int dtype, int batch, int chi_cap, const void* cores_a, const int32_t* bonds_a,
+                      const void* cores_b, const int32_t* bonds_b, void* out, void* stream);
 
 /* Measured FP64 FMA throughput of this GPU (the roofline denominator of the complex128 path). */
 tq_status tq_tt_dfma_peak(int32_t iters, void* stream, double* tflops_out);

@@ -105,10 +105,14 @@ def load(path: str | None = None):
         lib.tq_tt_tape_bytes.argtypes = [i32, i32, i32, i32]
         lib.tq_tt_taped.restype = i32
         lib.tq_tt_taped.argtypes = [i32, vp, i32, i32, i32, i32, vp, i64, ctypes.c_double, i32, i32,
-                                    vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+                                    vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
         lib.tq_tt_replay.restype = i32
         lib.tq_tt_replay.argtypes = [i32, vp, i32, i32, i32, i32, vp, i64, i32, vp, i32, vp,
-                                     vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+                                     vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        lib.tq_tt_apply.restype = i32
+        lib.tq_tt_apply.argtypes = [i32, vp, i32, i32, i32, vp, i64, ctypes.c_double, i32, i32, vp, vp, vp, vp, vp, vp]
+        lib.tq_tt_inner.restype = i32
+        lib.tq_tt_inner.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
         lib.tq_tt_dfma_peak.restype = i32
         lib.tq_tt_dfma_peak.argtypes = [i32, vp, ctypes.POINTER(ctypes.c_double)]
         _lib = lib
@@ -120,7 +124,7 @@ EXPORTED_SYMBOLS = ("tq_workspace_bytes", "tq_energy_grad", "tq_energy_grad_time
                     "tq_status_string", "tq_last_error", "tq_abi_layout", "tq_build_info",
                     "tq_tt_workspace_bytes", "tq_tt_simulate", "tq_tt_dfma_peak", "tq_tt_state_bytes",
                     "tq_tt_values_workspace_bytes", "tq_tt_run", "tq_tt_compress", "tq_tt_values",
-                    "tq_tt_tape_bytes", "tq_tt_taped", "tq_tt_replay")
+                    "tq_tt_tape_bytes", "tq_tt_taped", "tq_tt_replay", "tq_tt_inner", "tq_tt_apply")
 
 
 def check(status: int):

@@ -222,6 +222,37 @@ def evaluate_expval(circuit: Circuit, ham: PauliHamiltonian, theta=None, engine:
     return float(v[0]) if single else v
 
 
+def expval_state(circuit: Circuit, ham: PauliHamiltonian, theta, state, *, want_grad: bool = True,
+                 dtype: str = "complex128", device=None):
+    """<state|U(theta)^H H U(theta)|state> and its exact gradient for an ARBITRARY input train
+    (a reference TTState's cores, tt.py:38-76, or a truncated.GPUTrain): the reference's expval on
+    any TTState (hamiltonians.py:167-187) with the circuit applied first.  Runs the taped
+    truncated engine from that train with eps = 0 and no bond cap, where every split keeps a
+    square unitary factor, so the frozen-constant shift rule is the exact gradient
+    (autodiff.py:8-13; truncated.straight_through).  Bonds above 32 raise BondTooLarge.
+
+    1-D theta -> (float, float64[P] | None); 2-D [B, P] -> (float64[B], float64[B, P] | None)."""
+    from . import truncated as TR
+
+    arr, single = _check_theta(circuit, theta)
+    terms = _terms(ham, circuit.n_qubits)
+    train = state if isinstance(state, TR.GPUTrain) else TR.GPUTrain.from_cores(
+        list(getattr(state, "cores", state)), dtype=dtype, device=_device(device))
+    vals, grad = TR.straight_through(circuit, terms, arr, 0.0, None, dtype=dtype, device=device,
+                                     want_grad=want_grad, init=train.row(0) if train.batch > 1 else train)
+    e = vals @ np.array([c for c, _ in terms], dtype=complex) if terms else np.zeros(arr.shape[0], complex)
+    if not (np.all(np.isfinite(e)) and (grad is None or np.all(np.isfinite(grad)))):
+        from .errors import NotFinite
+        raise NotFinite("engine produced NaN or Inf")
+    tol = E.residue_tol(dtype, sum(abs(c) for c, _ in terms))
+    if e.size and float(np.max(np.abs(e.imag))) > tol:
+        from .errors import NonHermitianResidue
+        raise NonHermitianResidue(f"imaginary residue {float(np.max(np.abs(e.imag))):.3e} exceeds {tol:.0e}")
+    if single:
+        return float(e.real[0]), (None if grad is None else grad[0])
+    return e.real, grad
+
+
 def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", *, dtype: str = "complex64",
                        device=None, segments=None):
     """Complex <P> per op-group sharing one state per theta-set (the values of

@@ -94,6 +94,11 @@ struct Params {
   struct TapeMeta* meta;
   const int32_t* parent;   // PH_REPLAY: the recorded theta-set whose tape row b replays
   int32_t n2;              // two-site gates in the program (tape slots per theta-set)
+  // optional input train (one train shared by every row, slot layout [n][2 cap^2], bonds [n+1]):
+  // PH_RUN starts from it instead of |0...0>
+  const void* init_cores;
+  const int32_t* init_bonds;
+  int32_t inplace;         // PH_RUN continues from the trains already in cores / bonds / centers
 };
 
 struct TapeMeta { int32_t k; int32_t left_iso; double scale; };
@@ -737,14 +742,24 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
   int32_t* flag = p.flags + b;
   if constexpr ((PHASE & PH_RUN) != 0) {
   const R* theta_b = reinterpret_cast<const R*>(p.theta) + (int64_t)b * p.theta_stride;
-  // |0...0>: bond 1 everywhere
-  for (int k = tid; k < n; k += NT) {
-    cores[(size_t)k * SLOT + 0] = cmk<C>(R(1), R(0));
-    cores[(size_t)k * SLOT + 1] = cmk<C>(R(0), R(0));
+  if (p.inplace) {
+    // the row's own train (cores, dims and centre as the caller left them) is the input state
+  } else if (p.init_cores) {   // a caller's train (reference TTState) as the input state
+    const C* src = reinterpret_cast<const C*>(p.init_cores);
+    for (int k = 0; k < n; ++k) {
+      const int cnt = p.init_bonds[k] * 2 * p.init_bonds[k + 1];
+      for (int e = tid; e < cnt; e += NT) cores[(size_t)k * SLOT + e] = src[(size_t)k * SLOT + e];
+    }
+    for (int k = tid; k <= n; k += NT) dims[k] = p.init_bonds[k];
+  } else {   // |0...0>: bond 1 everywhere
+    for (int k = tid; k < n; k += NT) {
+      cores[(size_t)k * SLOT + 0] = cmk<C>(R(1), R(0));
+      cores[(size_t)k * SLOT + 1] = cmk<C>(R(0), R(0));
+    }
+    for (int k = tid; k <= n; k += NT) dims[k] = 1;
   }
-  for (int k = tid; k <= n; k += NT) dims[k] = 1;
   __syncthreads();
-  int center = 0;
+  int center = (p.inplace && p.centers) ? p.centers[b] : 0;
   double disc = 0.0;
   constexpr bool TAPED = (PHASE & (PH_TAPE | PH_REPLAY)) != 0;
   constexpr int TSLOT = 2 * CAP * CAP;
@@ -793,7 +808,10 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
     two_site<R, CAP>(s, p, cores, dims, site, disc, flag);
     center = m <= nn ? site + 1 : site;
   }
-  if (tid == 0) { if (p.discarded) p.discarded[b] = disc; if (p.centers) p.centers[b] = center; }
+  if (tid == 0) {
+    if (p.discarded) p.discarded[b] = (p.inplace ? p.discarded[b] : 0.0) + disc;   // in place: accumulates
+    if (p.centers) p.centers[b] = center;
+  }
   __syncthreads();
   }
   if constexpr ((PHASE & PH_COMPRESS) != 0) {
@@ -856,6 +874,50 @@ __global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
     if (tid == 0) p.values[(size_t)b * p.n_terms + t] = make_double2(red_re[0], red_im[0]);
     __syncthreads();
   }
+}
+
+// <a_b|b_b> of two trains per batch row (reference tt_inner, tt.py:247-255): left-to-right
+// transfer env' = sum_s A_s^H env B_s, A conjugated.  One CTA per row.
+template <typename R, int CAP>
+__global__ void __launch_bounds__(NT, 1) tt_inner_kernel(int n, const void* cores_a, const int32_t* bonds_a,
+                                                         const void* cores_b, const int32_t* bonds_b, double2* out) {
+  using C = typename CT<R>::T;
+  constexpr int SLOT = 2 * CAP * CAP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ_SMEM_POISON(smem_raw);
+  Scratch<R, CAP>& s = *reinterpret_cast<Scratch<R, CAP>*>(smem_raw);
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const C* A = reinterpret_cast<const C*>(cores_a) + (size_t)row * n * SLOT;
+  const C* B = reinterpret_cast<const C*>(cores_b) + (size_t)row * n * SLOT;
+  const int32_t* da = bonds_a + (size_t)row * (n + 1);
+  const int32_t* db = bonds_b + (size_t)row * (n + 1);
+  C* env = s.V;                 // [ca][cb]
+  C* T = s.X;                   // [ca][(s, d)]
+  if (tid == 0) env[0] = cmk<C>(R(1), R(0));
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int ca = da[k], cb = db[k], ca2 = da[k + 1], cb2 = db[k + 1];
+    const C* Ak = A + (size_t)k * SLOT;
+    const C* Bk = B + (size_t)k * SLOT;
+    const int w = 2 * cb2;
+    for (int e = tid; e < ca * w; e += NT) {      // T[a][(s, d)] = sum_b env[a][b] B[b][s][d]
+      const int a = e / w, col = e - a * w;
+      C acc = cmk<C>(R(0), R(0));
+      for (int bb = 0; bb < cb; ++bb) cfma(acc, env[a * cb + bb], Bk[bb * w + col]);
+      T[e] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < ca2 * cb2; e += NT) {   // env'[c][d] = sum_{a,s} conj(A[a][s][c]) T[a][(s, d)]
+      const int c = e / cb2, d = e - c * cb2;
+      C acc = cmk<C>(R(0), R(0));
+      for (int a = 0; a < ca; ++a)
+#pragma unroll
+        for (int sp = 0; sp < 2; ++sp) cfmac(acc, Ak[(a * 2 + sp) * ca2 + c], T[a * w + sp * cb2 + d]);
+      env[e] = acc;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) out[row] = make_double2(double(env[0].x), double(env[0].y));
 }
 
 template <typename R, int CAP, int PHASE>
@@ -1031,6 +1093,21 @@ tq_status tq_tt_run(int n_qubits, const void* gates, int n_gates, int dtype, int
   return dispatch<PH_RUN>(p, dtype, st);
 }
 
+tq_status tq_tt_apply(int n_qubits, const void* gates, int n_gates, int dtype, int batch, const void* theta,
+                      int64_t theta_stride, double eps, int chi_cap, int chi_max, void* cores, int32_t* bonds,
+                      int32_t* centers, double* discarded, int32_t* flags, void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_apply", n_qubits, batch, chi_cap, dtype) || n_gates < 0) return TQ_ERR_INPUT;
+  Params p{};
+  p.n = n_qubits; p.n_gates = n_gates; p.batch = batch; p.chi_cap = chi_cap; p.chi_max = chi_max;
+  p.gates = reinterpret_cast<const tq_tgate*>(gates); p.theta = theta; p.theta_stride = theta_stride;
+  p.eps = eps; p.bonds = bonds; p.flags = flags; p.centers = centers; p.cores = cores; p.inplace = 1;
+  p.discarded = discarded;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
+  return dispatch<PH_RUN>(p, dtype, st);
+}
+
 tq_status tq_tt_compress(int n_qubits, int dtype, int batch, double eps, int chi_cap, int chi_max, void* cores,
                          int32_t* bonds, int32_t* centers, double* discarded, int32_t* flags, void* stream) {
   using namespace tqt;
@@ -1058,6 +1135,7 @@ static tq_status tt_taped_common(int phase, int n_qubits, const void* gates, int
                                  int chi_max, const int32_t* parent, const int32_t* term_lo, const int32_t* term_hi,
                                  const int32_t* code_off, const int8_t* codes, int n_terms, void* values,
                                  double* norm2, int32_t* bonds, int32_t* flags, void* tape, int tape_batch,
+                                 const void* init_cores, const int32_t* init_bonds,
                                  void* workspace, size_t workspace_bytes, void* stream) {
   using namespace tqt;
   if (bad_sizes("tq_tt_taped", n_qubits, batch, chi_cap, dtype) || n_gates < 0 || n_terms < 0 || n_two_site < 0)
@@ -1081,6 +1159,7 @@ static tq_status tt_taped_common(int phase, int n_qubits, const void* gates, int
   p.tape = tape;
   p.meta = reinterpret_cast<TapeMeta*>(reinterpret_cast<unsigned char*>(tape) + align256(slots * 2 * c * c * csz));
   p.parent = parent; p.n2 = n_two_site;
+  p.init_cores = init_cores; p.init_bonds = init_bonds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(flags, 0, sizeof(int32_t) * batch, st);
   return phase == PH_TAPE ? dispatch<PH_RUN | PH_TAPE | PH_VALUES>(p, dtype, st)
@@ -1091,20 +1170,52 @@ tq_status tq_tt_taped(int n_qubits, const void* gates, int n_gates, int n_two_si
                       const void* theta, int64_t theta_stride, double eps, int chi_cap, int chi_max,
                       const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off, const int8_t* codes,
                       int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags, void* tape,
+                      const void* init_cores, const int32_t* init_bonds,
                       void* workspace, size_t workspace_bytes, void* stream) {
   return tt_taped_common(tqt::PH_TAPE, n_qubits, gates, n_gates, n_two_site, dtype, batch, theta, theta_stride, eps,
                          chi_cap, chi_max, nullptr, term_lo, term_hi, code_off, codes, n_terms, values, norm2, bonds,
-                         flags, tape, batch, workspace, workspace_bytes, stream);
+                         flags, tape, batch, init_cores, init_bonds, workspace, workspace_bytes, stream);
 }
 
 tq_status tq_tt_replay(int n_qubits, const void* gates, int n_gates, int n_two_site, int dtype, int rows,
                        const void* theta, int64_t theta_stride, int chi_cap, const int32_t* parent, int tape_batch,
                        const void* tape, const int32_t* term_lo, const int32_t* term_hi, const int32_t* code_off,
                        const int8_t* codes, int n_terms, void* values, double* norm2, int32_t* bonds, int32_t* flags,
+                       const void* init_cores, const int32_t* init_bonds,
                        void* workspace, size_t workspace_bytes, void* stream) {
   return tt_taped_common(tqt::PH_REPLAY, n_qubits, gates, n_gates, n_two_site, dtype, rows, theta, theta_stride, 0.0,
                          chi_cap, -1, parent, term_lo, term_hi, code_off, codes, n_terms, values, norm2, bonds, flags,
-                         const_cast<void*>(tape), tape_batch, workspace, workspace_bytes, stream);
+                         const_cast<void*>(tape), tape_batch, init_cores, init_bonds, workspace, workspace_bytes,
+                         stream);
+}
+
+tq_status tq_tt_inner(int n_qubits, int dtype, int batch, int chi_cap, const void* cores_a, const int32_t* bonds_a,
+                      const void* cores_b, const int32_t* bonds_b, void* out, void* stream) {
+  using namespace tqt;
+  if (bad_sizes("tq_tt_inner", n_qubits, batch, chi_cap, dtype)) return TQ_ERR_INPUT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int c = cap_bucket(chi_cap);
+  double2* o = reinterpret_cast<double2*>(out);
+#define TQ_INNER(R, CAPV)                                                                                         \
+  {                                                                                                               \
+    const size_t smem = sizeof(Scratch<R, CAPV>);                                                                 \
+    cudaFuncSetAttribute(tt_inner_kernel<R, CAPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    tt_inner_kernel<R, CAPV><<<batch, NT, smem, st>>>(n_qubits, cores_a, bonds_a, cores_b, bonds_b, o);          \
+  }
+  if (dtype == TQ_C128) {
+    if (c <= 4) TQ_INNER(double, 4) else if (c <= 8) TQ_INNER(double, 8) else if (c <= 16) TQ_INNER(double, 16)
+    else TQ_INNER(double, 32)
+  } else {
+    if (c <= 4) TQ_INNER(float, 4) else if (c <= 8) TQ_INNER(float, 8) else if (c <= 16) TQ_INNER(float, 16)
+    else TQ_INNER(float, 32)
+  }
+#undef TQ_INNER
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(tq::g_err, sizeof(tq::g_err), "%s", cudaGetErrorString(e));
+    return TQ_ERR_CUDA;
+  }
+  return TQ_OK;
 }
 
 size_t tq_tt_values_workspace_bytes(int n_qubits, int batch, int chi_cap, int dtype) {

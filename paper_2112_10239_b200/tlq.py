@@ -31,7 +31,7 @@ from .errors import InputError, SizeMismatch
 from .hamiltonians import PauliHamiltonian, PauliTerm
 
 __all__ = ["RotX", "RotY", "RotZ", "cnot", "cz", "Unitary", "UnaryGatesUnitary", "BinaryGatesUnitary",
-           "TTCircuit", "ProductState", "spins_to_tt_state", "pauli_x", "pauli_y", "pauli_z",
+           "TTCircuit", "ProductState", "TTState", "spins_to_tt_state", "pauli_x", "pauli_y", "pauli_z",
            "unary_hamiltonian", "binary_hamiltonian", "ising_hamiltonian", "maxcut_readouts"]
 
 
@@ -145,6 +145,46 @@ class ProductState:
         return bool(np.all(self.vectors[:, 0] == 1) and np.all(self.vectors[:, 1] == 0))
 
 
+class TTState:
+    """An arbitrary tensor-train input state: n cores of shape (chi_l, 2, chi_r) (the reference's
+    TTState.cores, tt.py:38-76; bonds <= 32).  TTCircuit.forward_expectation_value on it is
+    differentiable (exact gradient, autodiff.expval_state); state_inner_product accepts it too."""
+
+    def __init__(self, cores):
+        self.cores = [np.asarray(c, dtype=complex) for c in getattr(cores, "cores", cores)]
+        if not self.cores or any(c.ndim != 3 or c.shape[1] != 2 for c in self.cores):
+            raise InputError("a TT state needs cores of shape (chi_l, 2, chi_r)")
+
+    @property
+    def nqubits(self) -> int:
+        return len(self.cores)
+
+    @classmethod
+    def from_product(cls, state: "ProductState") -> "TTState":
+        return cls([v.reshape(1, 2, 1) for v in state.vectors])
+
+
+class _TrainExpval(torch.autograd.Function):
+    """E[b] on an arbitrary input train; gradient from the same engine calls (exact shift rule on
+    frozen-constant replays, truncated.straight_through)."""
+
+    @staticmethod
+    def forward(ctx, theta, circuit, ham, state):
+        from .autodiff import expval_state
+
+        want = bool(ctx.needs_input_grad[0])
+        e, g = expval_state(circuit, ham, theta.detach().double().cpu().numpy(), state.cores, want_grad=want,
+                            device=theta.device if theta.is_cuda else None)
+        if want:
+            ctx.save_for_backward(torch.as_tensor(g, dtype=theta.dtype, device=theta.device))
+        return torch.as_tensor(e, dtype=torch.float64, device=theta.device)
+
+    @staticmethod
+    def backward(ctx, g_e):
+        (g,) = ctx.saved_tensors
+        return (g_e.to(g.dtype)[:, None] * g), None, None, None
+
+
 def spins_to_tt_state(spins) -> ProductState:
     """|s_0 s_1 ...> for bits s_i (qubit 0 most significant)."""
     vecs = np.zeros((len(spins), 2), dtype=complex)
@@ -200,6 +240,13 @@ class TTCircuit(nn.Module):
         if operator.n_qubits != self.nqubits:
             raise SizeMismatch(f"operator on {operator.n_qubits} qubits, circuit {self.nqubits}")
         dev = self._dev()
+        if isinstance(state, TTState):   # an arbitrary train: the taped engine from that state
+            if state.nqubits != self.nqubits:
+                raise SizeMismatch("state and circuit qubit counts differ")
+            single = theta is None
+            th = self.theta().to(dev)[None] if single else theta.to(dev)
+            val = _TrainExpval.apply(th, self._circuit, operator, state)
+            return val[0] if single else val
         init = None if state is None or state.is_zero() else state.vectors
         if state is not None and state.nqubits != self.nqubits:
             raise SizeMismatch("state and circuit qubit counts differ")
@@ -220,6 +267,20 @@ class TTCircuit(nn.Module):
         rotation parameters (exact shift rule, one batched launch; autodiff.InnerFunction)."""
         from .autodiff import inner
 
+        if isinstance(state, TTState) or isinstance(compare_state, TTState):
+            # arbitrary trains: the circuit applied to the ket train on the truncated engine (no
+            # truncation), then the train-train transfer <compare|U|state> (forward only)
+            from . import truncated as TR
+
+            def train(s):
+                if s is None:
+                    s = spins_to_tt_state([0] * self.nqubits)
+                s = s if isinstance(s, TTState) else TTState.from_product(s)
+                return TR.GPUTrain.from_cores(s.cores, dtype="complex128", device=self._dev())
+
+            ket = TR.apply_circuit(train(state), self._circuit, self.theta().detach().double().cpu().numpy())
+            z = TR.tt_inner(train(compare_state), ket)[0]
+            return torch.tensor(complex(z), dtype=torch.complex128, device=self._dev())
         ki = None if state is None else state.vectors
         bi = None if compare_state is None else compare_state.vectors
         th = self.theta().to(self._dev())

@@ -302,6 +302,59 @@ class GPUTrain:
             c <<= 1
         return 2 * c * c
 
+    @classmethod
+    def from_cores(cls, trains, *, dtype: str = "complex128", device=None, cap: int | None = None) -> "GPUTrain":
+        """Device trains from reference-layout cores: ``trains`` is one list of (chi_l, 2, chi_r)
+        arrays (a reference TTState's ``cores``, tt.py:38-76) or a list of such lists (a batch)."""
+        import torch
+
+        from .autodiff import _device
+
+        if trains and isinstance(trains[0], np.ndarray) and np.asarray(trains[0]).ndim == 3:
+            trains = [trains]
+        trains = [[np.asarray(c, dtype=complex) for c in tr] for tr in trains]
+        n = len(trains[0])
+        if n < 1 or any(len(tr) != n for tr in trains):
+            raise InputError("trains must be non-empty and of equal length")
+        chi = 1
+        for tr in trains:
+            for k, c in enumerate(tr):
+                if c.ndim != 3 or c.shape[1] != 2:
+                    raise InputError(f"core {k} must have shape (chi_l, 2, chi_r), got {c.shape}")
+                if k and tr[k - 1].shape[2] != c.shape[0]:
+                    raise InputError(f"bond mismatch between cores {k - 1} and {k}")
+                chi = max(chi, c.shape[0], c.shape[2])
+            if tr[0].shape[0] != 1 or tr[-1].shape[2] != 1:
+                raise InputError("the boundary bonds of a train must be 1")
+        cap = max(int(cap or 1), chi)
+        if cap > MAX_CHI_TRUNC:
+            raise BondTooLarge(f"a train bond of {chi} exceeds the engine's capacity {MAX_CHI_TRUNC}")
+        out = cls(n, len(trains), cap, dtype, _device(device))
+        cdt = torch.complex128 if dtype == "complex128" else torch.complex64
+        slot = out._slot()
+        host = np.zeros((len(trains), n, slot), dtype=np.complex128)
+        bonds = np.ones((len(trains), n + 1), dtype=np.int32)
+        for b, tr in enumerate(trains):
+            for k, c in enumerate(tr):
+                host[b, k, : c.size] = c.reshape(-1)
+                bonds[b, k], bonds[b, k + 1] = c.shape[0], c.shape[2]
+        out.cores.view(cdt).copy_(torch.from_numpy(host.reshape(-1)).to(cdt))
+        out.bonds.copy_(torch.from_numpy(bonds))
+        return out
+
+    def row(self, b: int) -> "GPUTrain":
+        """Train b alone (a copy with batch 1)."""
+        out = GPUTrain.__new__(GPUTrain)
+        out.__dict__.update(self.__dict__)
+        nbytes = self.cores.numel() // self.batch
+        out.batch = 1
+        out.cores = self.cores[b * nbytes:(b + 1) * nbytes].clone()
+        out.bonds = self.bonds[b:b + 1].clone()
+        out.centers = self.centers[b:b + 1].clone()
+        out.discarded = self.discarded[b:b + 1].clone()
+        out.flags = self.flags[b:b + 1].clone()
+        return out
+
     def clone(self) -> "GPUTrain":
         out = GPUTrain.__new__(GPUTrain)
         out.__dict__.update(self.__dict__)
@@ -385,6 +438,65 @@ def simulate_train(circuit: Circuit, theta, eps: float = 0.0, chi_max=None, *, d
     return train.check()
 
 
+def apply_circuit(train: GPUTrain, circuit: Circuit, theta, eps: float = 0.0, chi_max=None) -> GPUTrain:
+    """Run ``circuit`` on trains the caller already holds (the reference's apply_gate_tt over every
+    gate, tt.py:186-234): a new train per row; the discarded weight accumulates onto the input's.
+    theta [B, P] (or [P] for every row)."""
+    import torch
+
+    from . import _lib
+    from .engine import _stream
+
+    if circuit.n_qubits != train.n:
+        from .errors import SizeMismatch
+        raise SizeMismatch(f"circuit on {circuit.n_qubits} qubits, train on {train.n}")
+    check_truncation_args(eps, chi_max)
+    theta = np.atleast_2d(np.asarray(theta, dtype=float))
+    if theta.shape[1] != circuit.n_params:
+        from .errors import ParamCountMismatch
+        raise ParamCountMismatch(f"{theta.shape[1]} parameters supplied, circuit has {circuit.n_params} slots")
+    if theta.shape[0] == 1 and train.batch > 1:
+        theta = np.repeat(theta, train.batch, axis=0)
+    cap = MAX_CHI_TRUNC if chi_max is None else max(int(chi_max), train.cap)
+    if cap > train.cap:   # room for the bonds the circuit grows (re-laid at the larger slot)
+        out = GPUTrain.from_cores([train.cores_host(r) for r in range(train.batch)], dtype=train.dtype,
+                                  device=train.device, cap=cap)
+        out.centers.copy_(train.centers)
+        out.discarded.copy_(train.discarded)
+    else:
+        out = train.clone()
+    table, d_gates = _device_gates(circuit, out.device)
+    th = torch.tensor(theta, dtype=torch.float64 if out.dtype == "complex128" else torch.float32, device=out.device)
+    _lib.check(_lib.load().tq_tt_apply(out.n, d_gates.data_ptr(), len(table), out.code, out.batch, th.data_ptr(),
+                                       th.stride(0), ctypes.c_double(eps), out.cap,
+                                       -1 if chi_max is None else int(chi_max), out.cores.data_ptr(),
+                                       out.bonds.data_ptr(), out.centers.data_ptr(), out.discarded.data_ptr(),
+                                       out.flags.data_ptr(), _stream()))
+    return out.check()
+
+
+def tt_inner(a: GPUTrain, b: GPUTrain) -> np.ndarray:
+    """<a_r|b_r> for every row of two train batches (reference tt_inner, tt.py:247-255), complex [B]."""
+    import torch
+
+    from . import _lib
+    from .engine import _stream
+
+    if a.n != b.n:
+        from .errors import SizeMismatch
+        raise SizeMismatch(f"{a.n} vs {b.n} qubits")
+    if a.batch != b.batch or a.dtype != b.dtype:
+        raise InputError("inner product needs trains of equal batch and dtype")
+    if a._slot() != b._slot():   # one slot layout for both (re-laid at the larger capacity)
+        cap = max(a.cap, b.cap)
+        a = GPUTrain.from_cores([a.cores_host(r) for r in range(a.batch)], dtype=a.dtype, device=a.device, cap=cap)
+        b = GPUTrain.from_cores([b.cores_host(r) for r in range(b.batch)], dtype=b.dtype, device=b.device, cap=cap)
+    out = torch.zeros(a.batch, 2, dtype=torch.float64, device=a.device)
+    _lib.check(_lib.load().tq_tt_inner(a.n, a.code, a.batch, a.cap, a.cores.data_ptr(), a.bonds.data_ptr(),
+                                       b.cores.data_ptr(), b.bonds.data_ptr(), out.data_ptr(), _stream()))
+    return torch.view_as_complex(out).cpu().numpy()
+
+
 def compress(train: GPUTrain, eps: float, chi_max=None) -> GPUTrain:
     """Re-truncate every bond of every train (reference compress, tt.py:299-320): a new train;
     the discarded weight accumulates onto the input's."""
@@ -412,7 +524,8 @@ def _check_flags(flags, cap):
 
 
 def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=None, *, dtype: str = "complex128",
-                     device=None, want_grad: bool = True, rows_per_launch: int | None = None):
+                     device=None, want_grad: bool = True, rows_per_launch: int | None = None,
+                     init: "GPUTrain | None" = None, weights=None):
     """The reference's gradient through truncated splits (``grad_expval`` with eps > 0 or a binding
     chi_max, autodiff.py:315-363,471-487): value and straight-through gradient for every theta-set.
 
@@ -425,8 +538,14 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
        rule on the replayed values: (E(t + pi/2) - E(t - pi/2)) / 2, and crz's four-term rule
        (autodiff.py:509-550).  Shifted rows are batched over the SMs, one CTA per row.
 
-    Returns (values [B, T] complex128 of the taped state, grad [B, P] float64 of
-    E = Re sum_t c_t v_t) -- the gradient needs the coefficients, so ``terms`` carry them."""
+    ``init``: an input train (batch 1, shared by every theta-set) instead of |0...0>.  With eps = 0
+    and no binding chi_max every split keeps a square unitary factor, so the result is the EXACT
+    gradient of <init|U^H H U|init> (the differentiable path for arbitrary input trains).
+    ``weights``: callable(values [B, T]) -> [B, T] cotangent weights w; the gradient is then that
+    of Re sum_t w_t v_t with w frozen at the unshifted values (the chain rule through a function
+    of the readouts, e.g. the MBE loss).  Default: the terms' coefficients (the energy).
+
+    Returns (values [B, T] complex128 of the taped state, grad [B, P] float64)."""
     import torch
 
     from . import _lib
@@ -448,6 +567,15 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
     lib = _lib.load()
     T = len(terms)
     coef = np.array([c for c, _ in terms], dtype=complex)
+    if init is not None:
+        if init.n != n or init.dtype != dtype:
+            raise InputError("the input train must match the circuit width and dtype")
+        cap = max(cap, init.cap) if chi_max is None else cap
+        if init._slot() != 2 * (1 << max(2, (cap - 1).bit_length())) ** 2 or init.batch != 1:
+            init = GPUTrain.from_cores(init.cores_host(0), dtype=dtype, device=dev, cap=cap)
+        init_ptrs = (init.cores.data_ptr(), init.bonds.data_ptr())
+    else:
+        init_ptrs = (None, None)
     tape = torch.empty(int(lib.tq_tt_tape_bytes(n2, B, cap, code)), dtype=torch.uint8, device=dev)
 
     def run(rows_theta, parent=None):
@@ -464,13 +592,14 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
                                  ctypes.c_double(eps), cap, -1 if chi_max is None else int(chi_max),
                                  d_lo.data_ptr(), d_hi.data_ptr(), d_offs.data_ptr(), d_codes.data_ptr(), T,
                                  values.data_ptr(), norm2.data_ptr(), bonds.data_ptr(), flags.data_ptr(),
-                                 tape.data_ptr(), ws.data_ptr(), ctypes.c_size_t(wsb), _stream())
+                                 tape.data_ptr(), *init_ptrs, ws.data_ptr(), ctypes.c_size_t(wsb), _stream())
         else:
             par = torch.tensor(parent, dtype=torch.int32, device=dev)
             st = lib.tq_tt_replay(n, d_gates.data_ptr(), len(table), n2, code, R_, th.data_ptr(), th.stride(0), cap,
                                   par.data_ptr(), B, tape.data_ptr(), d_lo.data_ptr(), d_hi.data_ptr(),
                                   d_offs.data_ptr(), d_codes.data_ptr(), T, values.data_ptr(), norm2.data_ptr(),
-                                  bonds.data_ptr(), flags.data_ptr(), ws.data_ptr(), ctypes.c_size_t(wsb), _stream())
+                                  bonds.data_ptr(), flags.data_ptr(), *init_ptrs, ws.data_ptr(), ctypes.c_size_t(wsb),
+                                  _stream())
         _lib.check(st)
         _check_flags(flags, cap)
         return torch.view_as_complex(values).cpu().numpy()[:, :T]
@@ -478,6 +607,7 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
     vals = run(theta)
     if not want_grad:
         return vals, None
+    W = np.broadcast_to(coef[None, :], vals.shape) if weights is None else np.asarray(weights(vals))
     names = [circuit.gates[g].name for g in circuit.trainable]
     rows, plan = [], []
     for b in range(B):
@@ -501,7 +631,8 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
     for c0 in range(0, len(rows), rows_per_launch):
         chunk = rows[c0:c0 + rows_per_launch]
         v = run(np.stack([t for _, t in chunk]), [b for b, _ in chunk])
-        e[c0:c0 + len(chunk)] = (v @ coef).real
+        par = np.array([b for b, _ in chunk])
+        e[c0:c0 + len(chunk)] = np.einsum("rt,rt->r", v, W[par]).real
     for b, k, idx in plan:
         if names[k] == "crz":
             grad[b, k] = _CRZ_Y1 * (e[idx[0]] - e[idx[1]]) - _CRZ_Y2 * (e[idx[2]] - e[idx[3]])
