@@ -96,6 +96,33 @@ def _truncating(circuit: Circuit, eps: float, chi_max) -> bool:
     return int(chi_max) < C.factored_chi(circuit.n_qubits, C.time_gates(circuit))
 
 
+def _taped_truncates(circuit: Circuit, eps: float, chi_max) -> bool:
+    """True when the reference's TAPED path (grad_expval / taped_expectations with eps, chi_max)
+    would cut a split: it keeps every singular value at eps = 0, zeros included, so its bonds are
+    min(2 chi_l, 2 chi_r) per split (no centre moves, _tt_taped_split autodiff.py:315-336) and can
+    exceed both the true Schmidt rank and the factored bond.  A cut that only drops zero singular
+    values leaves the state (and value) exact but freezes a non-square factor, so the gradient is
+    then the straight-through one, not the exact one.  eps > 0 may cut anywhere: True."""
+    if eps > 0:
+        return True
+    if chi_max is None:
+        return False
+    from . import truncated as TR
+
+    table, _ = TR.compile_gates(circuit)
+    dims = [1] * (circuit.n_qubits + 1)
+    cap = int(chi_max)
+    for g in table:
+        if g["kind"] != 2:
+            continue
+        i = int(g["site"])
+        k = min(2 * dims[i], 2 * dims[i + 2])
+        if k > cap:
+            return True
+        dims[i + 1] = k
+    return False
+
+
 def _truncated_expval(circuit, ham, arr, eps, chi_max, dtype, device):
     """Forward value through the truncated TT engine (reference simulate_tt + expval,
     tt.py:237-244 / hamiltonians.py:167-187), every theta-set of arr [B, P] in one launch."""
@@ -180,7 +207,7 @@ def grad_expval(circuit: Circuit, ham: PauliHamiltonian, theta, engine: str = "t
     1-D theta -> (float, float64[P]); 2-D theta [B,P] -> (float64[B], float64[B,P])."""
     eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, single = _check_theta(circuit, theta)
-    if _truncating(circuit, eps, chi_max):
+    if _truncating(circuit, eps, chi_max) or _taped_truncates(circuit, eps, chi_max):
         # the reference's straight-through gradient of its taped truncated state (autodiff.py:10-13,
         # 315-363): value of the taped construction and the gradient with the split constants frozen
         v, g = _straight_through(circuit, ham, arr, eps, chi_max, dtype if dtype != "complex64" else "complex128",

@@ -26,7 +26,7 @@ import torch
 
 from . import chain as C
 from . import engine as E
-from .autodiff import _check_engine, _device, _engine_args, _truncating, init_params
+from .autodiff import _check_engine, _device, _engine_args, _taped_truncates, _truncating, init_params
 from .circuits import Circuit, standard_gate
 from .errors import (
     DivergenceDetected,
@@ -275,25 +275,42 @@ class MBEObjective:
         return loss, grad
 
 
-def _exact_only(engine, circuit, eps, chi_max, what):
-    """engine seam + truncation arguments of the MBE entry points.  The B200 MBE path is the exact
-    engine; a truncating (eps, chi_max) is refused loudly rather than silently ignored."""
+def _truncation(engine, circuit, eps, chi_max):
+    """(eps, chi_max, truncating) of an MBE entry point after the engine seam.  A truncating run
+    follows the reference's taped truncated path (taped_expectations with eps / chi_max,
+    autodiff.py:405-425): readouts of the taped state, straight-through gradients
+    (truncated.straight_through)."""
     eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
-    if _truncating(circuit, eps, chi_max):
-        raise InputError(f"{what}: truncated (eps > 0 or binding chi_max) MBE runs are not supported by the "
-                         "B200 engine; use eps=0 and chi_max >= the exact bond")
+    return eps, chi_max, _truncating(circuit, eps, chi_max) or _taped_truncates(circuit, eps, chi_max)
+
+
+def _edge_loss_and_cotangents(graph: Graph, alpha: float, r: np.ndarray):
+    """L = sum w tanh(a r_u) tanh(a r_v) and dL/dr_u = a (1 - t_u^2) sum_(u,v,w) w t_v (host, float64)."""
+    t = np.tanh(alpha * r)
+    loss = sum(w * t[u] * t[v] for u, v, w in graph.edges)
+    g = np.zeros_like(r)
+    for u, v, w in graph.edges:
+        g[u] += w * t[v]
+        g[v] += w * t[u]
+    return float(loss), alpha * (1.0 - t * t) * g
 
 
 def vertex_expectations(circuit: Circuit, theta, graph: Graph, engine: str = "tt", eps: float = 0.0,
                         chi_max=None, *, dtype: str = "complex128", device=None):
     """Per-vertex readouts (reference maxcut.py:206-216); complex128 by default for exact rounding."""
-    _exact_only(engine, circuit, eps, chi_max, "vertex_expectations")
+    eps, chi_max, trunc = _truncation(engine, circuit, eps, chi_max)
     n, ham = _readout_terms(graph)
     if circuit.n_qubits != n:
         raise SizeMismatch(f"circuit has {circuit.n_qubits} qubits, encoding needs {n}")
     th = np.asarray(theta, dtype=float)
     single = th.ndim == 1
     th2 = th.reshape(1, -1) if single else th
+    if trunc:   # readouts of the taped truncated state
+        from . import truncated as TR
+
+        vals, _ = TR.straight_through(circuit, C.normalize_terms(ham), th2, eps, chi_max, dtype="complex128",
+                                      device=device, want_grad=False)
+        return vals.real[0] if single else vals.real
     dev = _device(device)
     dp = E.device_plan(circuit, C.normalize_terms(ham), "values", th2.shape[0], dev, None, dtype=dtype)
     vals = E.values_raw(dp, torch.tensor(th2, dtype=E.DTYPES[dtype][1], device=dev), dtype).real.cpu().numpy()
@@ -304,7 +321,9 @@ def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: st
                   chi_max=None, *, dtype: str = "complex128", device=None):
     """fun(theta) -> (loss, grad) (reference maxcut.py:219-252), one device round trip per call.
     complex128 by default, like the reference; ``dtype="complex64"`` is the fast path."""
-    _exact_only(engine, circuit, eps, chi_max, "mbe_objective")
+    eps, chi_max, trunc = _truncation(engine, circuit, eps, chi_max)
+    if trunc:
+        return _mbe_objective_truncated(circuit, graph, alpha, eps, chi_max, device)
     obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device)
     P = circuit.n_params
     # Host-buffer serving path: the first call runs eagerly; the second captures the whole
@@ -353,6 +372,40 @@ def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: st
         torch.cuda.current_stream(obj.device).synchronize()
         out = out_host.numpy()[0].copy()
         return float(out[0]), out[1:]
+
+    return fun
+
+
+def _mbe_objective_truncated(circuit: Circuit, graph: Graph, alpha: float, eps: float, chi_max, device):
+    """The reference's truncated MBE objective: readouts of the taped truncated state and the
+    straight-through gradient of the edge loss through them (the reference's one tape,
+    maxcut.py:219-252): the cotangents dL/dr_u weight the frozen-constant replays."""
+    from . import truncated as TR
+
+    n, ham = _readout_terms(graph)
+    if circuit.n_qubits != n:
+        raise SizeMismatch(f"circuit has {circuit.n_qubits} qubits, encoding needs {n}")
+    if not math.isfinite(alpha) or alpha <= 0:
+        raise InputError("alpha must be positive and finite")
+    terms = C.normalize_terms(ham)
+    P = circuit.n_params
+
+    def fun(theta):
+        th = np.asarray(theta, dtype=float).reshape(-1)
+        if th.shape[0] != P:
+            raise ParamCountMismatch(f"expected {P} parameters, got {th.shape[0]}")
+        if not np.all(np.isfinite(th)):
+            raise InputError("theta contains non-finite values")
+        out = {}
+
+        def weights(vals):
+            loss, g = _edge_loss_and_cotangents(graph, alpha, vals.real[0])
+            out["loss"] = loss
+            return g[None, :]
+
+        _, grad = TR.straight_through(circuit, terms, th[None], eps, chi_max, dtype="complex128", device=device,
+                                      weights=weights)
+        return out["loss"], grad[0]
 
     return fun
 
@@ -471,8 +524,9 @@ def solve_maxcut(graph: Graph, depth: int = 4, engine: str = "tt", eps: float = 
     compatibility (the batch replaces the reference's thread pool).  complex128 by default:
     the reference trains in complex128, and the trained angles (hence the rounded cut) follow
     its trajectory only at that precision (tests/test_gpu_f1.py)."""
+    trunc = False
     if graph.num_vertices and graph.edges:
-        _exact_only(engine, brickwork_ansatz(mbe_encode(graph)[0], depth), eps, chi_max, "solve_maxcut")
+        eps, chi_max, trunc = _truncation(engine, brickwork_ansatz(mbe_encode(graph)[0], depth), eps, chi_max)
     else:
         _check_engine(engine)
     if optimizer not in ("gd", "adam"):
@@ -483,10 +537,22 @@ def solve_maxcut(graph: Graph, depth: int = 4, engine: str = "tt", eps: float = 
         return MbeResult((1,) * graph.num_vertices, 0.0, 0.0, 0, 0, seed)
     n, _ = mbe_encode(graph)
     circuit = brickwork_ansatz(n, depth)
-    obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device, batch=restarts)
     theta0 = np.stack([init_params(circuit.n_params, rng) for rng in spawn(seed, restarts)])
-    theta, loss, iters = adam_batched(obj, theta0, rate, max_iters, optimizer=optimizer)
-    exps = vertex_expectations(circuit, theta, graph, device=obj.device)
+    if trunc:
+        # the reference's truncated runs: minimize on the taped objective per restart (host loop
+        # over device calls; autodiff.minimize = the reference's minimize, autodiff.py:614-659)
+        from .autodiff import minimize
+
+        fun = _mbe_objective_truncated(circuit, graph, alpha, eps, chi_max, device)
+        runs = [minimize(fun, theta0[r], optimizer=optimizer, rate=rate, max_iters=max_iters) for r in range(restarts)]
+        theta = np.stack([res.theta for res in runs])
+        loss = np.array([res.value for res in runs])
+        iters = np.array([res.n_iters for res in runs])
+        exps = vertex_expectations(circuit, theta, graph, eps=eps, chi_max=chi_max, device=device)
+    else:
+        obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device, batch=restarts)
+        theta, loss, iters = adam_batched(obj, theta0, rate, max_iters, optimizer=optimizer)
+        exps = vertex_expectations(circuit, theta, graph, device=obj.device)
     outcomes = []
     for r in range(restarts):
         asg = round_cut(exps[r])

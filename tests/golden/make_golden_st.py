@@ -138,8 +138,26 @@ def main():
         with SplitWatch(eps, chi) as w:
             rep = run_cli(argv)
         cli_runs.append({"argv": argv, "report": rep, "well_posed": w.ok})
+    # MBE MaxCut through truncated splits (maxcut.py:206-319 with eps / chi_max)
+    from tnsim.maxcut import Graph, brickwork_ansatz, mbe_objective, solve_maxcut, vertex_expectations
+    small = json.load(open(os.path.join(HERE, "golden_small.json")))["mbe10"]
+    graph = Graph(10, tuple((int(u), int(v), float(w)) for u, v, w in small["edges"]))
+    bw = brickwork_ansatz(5, small["depth"])
+    mbe = []
+    for eps, chi in ((0.0, 2), (0.15, None)):
+        with SplitWatch(eps, chi) as w:
+            loss, grad = mbe_objective(bw, graph, alpha=small["alpha"], engine="tt", eps=eps, chi_max=chi)(
+                np.array(small["theta"]))
+            ev = vertex_expectations(bw, np.array(small["theta"]), graph, engine="tt", eps=eps, chi_max=chi)
+            sol = solve_maxcut(graph, depth=small["depth"], engine="tt", eps=eps, chi_max=chi, restarts=2,
+                               max_iters=6, seed=3, alpha=small["alpha"])
+        mbe.append({"eps": eps, "chi_max": chi, "loss": loss, "grad": grad.tolist(), "vertex": ev.tolist(),
+                    "solve": {"assignment": list(sol.assignment), "cut": sol.cut_value, "loss": sol.relaxed_loss,
+                              "iters": sol.iterations, "restart_index": sol.restart_index},
+                    "well_posed": w.ok})
+        print("mbe", eps, chi, loss, w.ok, sol.cut_value)
     with open(os.path.join(HERE, "golden_st.json"), "w") as fh:
-        json.dump({"cases": cases, "cli": cli_runs}, fh)
+        json.dump({"cases": cases, "cli": cli_runs, "mbe": mbe}, fh)
     for c in cases:
         print(c["name"], c["value"], np.linalg.norm(c["grad"]), "well_posed", c["well_posed"], c["splits"])
     for r in cli_runs:

@@ -174,3 +174,28 @@ def test_straight_through_gradient_matches_reference():
     np.testing.assert_allclose(g2[0], case["grad"], atol=1e-9)
     v1, g1 = AD.grad_expval(c, h, th[1], eps=case["eps"], chi_max=case["chi_max"], dtype="complex128")
     np.testing.assert_allclose(g2[1], g1, atol=1e-12)
+
+
+def test_truncated_mbe_matches_reference(golden_small):
+    """MBE MaxCut through truncated splits (reference maxcut.py:206-319 with eps / chi_max): taped
+    readouts, the straight-through loss gradient and solve_maxcut end to end, against real-tnsim
+    goldens (make_golden_st.py; every run here is well posed)."""
+    from paper_2112_10239_b200 import maxcut as MC
+
+    with open(os.path.join(HERE, "golden", "golden_st.json")) as f:
+        runs = json.load(f)["mbe"]
+    d = golden_small["mbe10"]
+    graph = MC.Graph(10, tuple((int(u), int(v), float(w)) for u, v, w in d["edges"]))
+    bw = MC.brickwork_ansatz(5, d["depth"])
+    for r in runs:
+        assert r["well_posed"]
+        kw = {"eps": r["eps"], "chi_max": r["chi_max"]}
+        loss, grad = MC.mbe_objective(bw, graph, alpha=d["alpha"], **kw)(np.array(d["theta"]))
+        assert abs(loss - r["loss"]) < 1e-10, kw
+        np.testing.assert_allclose(grad, r["grad"], atol=1e-9, err_msg=str(kw))
+        ev = MC.vertex_expectations(bw, np.array(d["theta"]), graph, **kw)
+        np.testing.assert_allclose(ev, r["vertex"], atol=1e-10, err_msg=str(kw))
+        sol = MC.solve_maxcut(graph, depth=d["depth"], restarts=2, max_iters=6, seed=3, alpha=d["alpha"], **kw)
+        assert list(sol.assignment) == r["solve"]["assignment"] and sol.cut_value == r["solve"]["cut"]
+        assert sol.restart_index == r["solve"]["restart_index"] and sol.iterations == r["solve"]["iters"]
+        assert abs(sol.relaxed_loss - r["solve"]["loss"]) < 1e-9
