@@ -21,9 +21,11 @@
  *
  * All arrays are caller-owned device memory (the library never allocates);
  * the chain tables are built by the host compiler (paper_2112_10239_b200/chain.py)
- * and uploaded by the caller.  Calls are reentrant, hold no global mutable
- * state, run on the caller's stream and are deterministic (no float atomics,
- * fixed-order reductions).
+ * and uploaded by the caller.  Calls are reentrant, run on the caller's stream and
+ * are deterministic (no float atomics, fixed-order reductions).  The only process-wide
+ * state is a mutex-protected cache of each kernel's opened dynamic-shared-memory
+ * limit (it only grows, so it never changes a result; it saves a
+ * cudaFuncSetAttribute per launch) and the last error message (thread_local).
  *
  * dtype: TQ_C64 -> theta/coef/grad are float32, TQ_C128 -> float64.
  * energy / values outputs are always float64 (re, im) pairs.

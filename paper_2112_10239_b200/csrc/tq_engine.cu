@@ -427,6 +427,44 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
 }
 
 
+// The same fold with two pairs per thread walked in lockstep (CTA teams, chi >= 16: 1024 pairs
+// on 512 threads).  The column is a chain of dependent 2x2 matvecs; interleaving two
+// independent chains hides the shared-memory load and FMA latencies of each op.
+template <typename R, int LD, int TEAM>
+__device__ void fold_site2(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                           const int* ocode, typename CT<R>::T* A, int lcr) {
+  using C = typename CT<R>::T;
+  const int npair = st.chi_l * st.chi_r;
+  const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+  const C z = cmk<C>(R(0), R(0));
+  for (int pa = tid; pa < npair; pa += 2 * TEAM) {
+    const int pb = pa + TEAM;
+    const bool hb = pb < npair;
+    const int ala = pa >> lcr, bea = pa & (st.chi_r - 1);
+    const int alb = hb ? pb >> lcr : ala, beb = hb ? pb & (st.chi_r - 1) : bea;
+    C a0 = i0, a1 = i1, b0 = i0, b1 = i1;
+#pragma unroll 2
+    for (int oi = 0; oi < st.op_count; ++oi) {
+      const int c = ocode[oi];
+      const C* Ma = mres + 4 * (oc_lmat(c) + oc_digit(c, ala, bea));
+      const C* Mb = mres + 4 * (oc_lmat(c) + oc_digit(c, alb, beb));
+      const C ma0 = Ma[0], ma1 = Ma[1], ma2 = Ma[2], ma3 = Ma[3];
+      const C mb0 = Mb[0], mb1 = Mb[1], mb2 = Mb[2], mb3 = Mb[3];
+      C na0 = cmul(ma0, a0), nb0 = cmul(mb0, b0);
+      C na1 = cmul(ma2, a0), nb1 = cmul(mb2, b0);
+      cfma(na0, ma1, a1); cfma(nb0, mb1, b1);
+      cfma(na1, ma3, a1); cfma(nb1, mb3, b1);
+      a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
+    }
+    if (st.pass_count && !pass_ok(ch, st, ala, bea)) { a0 = z; a1 = z; }
+    A[ala * LD + bea] = a0; A[LD * LD + ala * LD + bea] = a1;
+    if (hb) {
+      if (st.pass_count && !pass_ok(ch, st, alb, beb)) { b0 = z; b1 = z; }
+      A[alb * LD + beb] = b0; A[LD * LD + alb * LD + beb] = b1;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ digit-tree column adjoint
 // The column's ops introduce bond digits one at a time, so after op l the distinct column
 // vectors are indexed by the digits introduced so far (toff_l + bits_l bits, the newest digit
@@ -638,11 +676,62 @@ __device__ __forceinline__ void pair_adjoint_warp(int nops, int al, int be, cons
 //   C_t[m x n] = sum_{q < nq} A_{t,q}[m x kk] * B_{t,q}[kk x n]   (all row stride LD)
 // Each item computes rt consecutive rows of one column; a warp's lanes walk columns so the
 // A operand is a broadcast and the B operand a contiguous row.
-template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, typename FA, typename FB, typename FS>
+template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, bool HERM = false, typename FA,
+          typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
   // CTA: the A operand is stored as X (kk x m) and used as X^H; CTB likewise for B (n x kk).
+  // HERM: every output C_t is Hermitian (m == n): only the tiles touching the upper triangle are
+  // computed and each strictly-upper element is stored twice, (i, j) and conj at (j, i).
   // (chi = 32 on the tensor pipe with 3xTF32 mma.sync was measured and reverted: its biased fp32
   // accumulation drifts the norm over long chains, profiles/r02_mma3_tf32_trial.txt)
+  if constexpr (HERM) {
+    if (LD >= 17 && m == n && n >= 16) {
+      // 4 rows x 2 adjacent columns per item, tiles (row block b, column pair c) with 2c + 1 >= 4b:
+      // 72 of 128 tiles at 32 x 32 (the environment transfers of the MPO sweeps are Hermitian:
+      // real coefficients, Hermitian Paulis)
+      const int nb = m >> 2, nc = n >> 1;
+      const int per = nb * nc - nb * (nb - 1);
+      const int total = ntasks * per;
+      for (int it = tid; it < total; it += TEAM) {
+        const int task = it / per;
+        int r = it - task * per, b = 0;
+        while (r >= nc - 2 * b) { r -= nc - 2 * b; ++b; }
+        const int i0 = b << 2, j0 = (2 * b + r) << 1;
+        C c00 = {0, 0}, c10 = {0, 0}, c20 = {0, 0}, c30 = {0, 0};
+        C c01 = {0, 0}, c11 = {0, 0}, c21 = {0, 0}, c31 = {0, 0};
+        for (int q = 0; q < nq; ++q) {
+          const C* Ab = fa(task, q) + (CTA ? i0 : i0 * LD);
+          const C* B0 = fb(task, q) + (CTB ? j0 * LD : j0);
+          const C* B1 = B0 + (CTB ? LD : 1);
+          const int sa = CTA ? LD : 1, ra = CTA ? 1 : LD, sb = CTB ? 1 : LD;
+#pragma unroll 4
+          for (int k = 0; k < kk; ++k) {
+            C b0 = B0[k * sb], b1 = B1[k * sb];
+            if (CTB) { b0 = cconj(b0); b1 = cconj(b1); }
+            const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
+            if (CTA) {
+              cfmac(c00, a0, b0); cfmac(c10, a1, b0); cfmac(c20, a2, b0); cfmac(c30, a3, b0);
+              cfmac(c01, a0, b1); cfmac(c11, a1, b1); cfmac(c21, a2, b1); cfmac(c31, a3, b1);
+            } else {
+              cfma(c00, a0, b0); cfma(c10, a1, b0); cfma(c20, a2, b0); cfma(c30, a3, b0);
+              cfma(c01, a0, b1); cfma(c11, a1, b1); cfma(c21, a2, b1); cfma(c31, a3, b1);
+            }
+          }
+        }
+        const C v[4][2] = {{c00, c01}, {c10, c11}, {c20, c21}, {c30, c31}};
+        const C z = {0, 0};
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int i = i0 + rr, j = j0 + cc;
+            if (j >= i) store(task, i, j, 1, v[rr][cc], z, z, z);
+            if (j > i) store(task, j, i, 1, cconj(v[rr][cc]), z, z, z);
+          }
+      }
+      return;
+    }
+  }
   if (LD >= 17 && n >= 16 && m >= 4) {
     // 4 rows x 2 columns (j, j + n/2) per item: 4 broadcast A loads + 2 B loads per 8 cMAC
     const int hn = n >> 1;
@@ -1072,7 +1161,8 @@ rl_sweep(Params p) {
     STAGE(0);
     // per-pair column walks: the digit-tree fold (levels in the dead N/BR slots) was measured
     // slower at chi = 32 (11.7k vs 7.7k cycles per site: 20 team barriers over small levels)
-    fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
+    if constexpr (TEAM >= 128) fold_site2<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, lcr);
+    else fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
     team_sync<TEAM>();
     if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
       C* ag = env_g + st.a_off;
@@ -1106,16 +1196,20 @@ rl_sweep(Params p) {
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     const bool store = p.store_env && st.env_out >= 0;
     C* envo = env_g + (store ? st.env_out : 0);
-    gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2,
-        [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
-        [&](int, int qq) { return sm.A + qq * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-          store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
-          if (store) {
-            C* h = envo + ((size_t)t << (2 * lcl)) + (i0 << lcl) + j;
-            h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
-          }
-        });
+    {
+      auto pa = [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; };
+      auto pb = [&](int, int qq) { return sm.A + qq * MS; };
+      auto ps = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
+        store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
+        if (store) {
+          C* h = envo + ((size_t)t << (2 * lcl)) + (i0 << lcl) + j;
+          h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
+        }
+      };
+      // the environments of the energy / gradient MPO are Hermitian (real coefficients): half the work
+      if (CHI >= 16 && p.mode == 0) gemm_group<C, LD, TEAM, false, true, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+      else gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+    }
     STAGE(5);
     // resolve the next site's descriptors while the GEMM above is in flight (independent work)
     int nx2 = -1;
@@ -1285,10 +1379,13 @@ lr_sweep(Params p) {
       STAGE(3);
     }
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
-    gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2,
-        [&](int, int qq) { return Acur + qq * MS; },
-        [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; },
-        [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+    {
+      auto la = [&](int, int qq) { return Acur + qq * MS; };
+      auto lb = [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; };
+      auto ls = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); };
+      if (CHI >= 16 && MODE == 0) gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
+      else gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2, la, lb, ls);
+    }
     int nx2 = -1;
     if (has_next) {   // next site's descriptors, overlapped with this site's GEMMs
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
