@@ -755,7 +755,7 @@ def f3_config(batch):
             "n_qubits": F3["n"], "gates": F3["gates"], "chi_max": F3["chi_max"], "eps": F3["eps"],
             "circuit": "tfim_workload: ry+rz rows and alternating cz lines, cut to the gate count",
             "operator": "TFIM open chain j=h=1 (all 999 term values)", "batch_per_gpu": batch,
-            "parallelism": "theta-set data parallel (one CTA per theta-set)",
+            "parallelism": "theta-set data parallel (one 128-thread CTA per theta-set, 4 resident per SM)",
             "l2": "flushed between timed steps (256 MiB memset, untimed)"}
 
 
@@ -806,7 +806,8 @@ def run_f3(args):
     dev = torch.device("cuda", local)
     circuit, terms = f3_problem()
     n, T = circuit.n_qubits, len(terms)
-    B = args.batch or torch.cuda.get_device_properties(dev).multi_processor_count
+    # four 128-thread CTAs (theta-sets) resident per SM (csrc/tq_trunc.cu NT): one wave of 4 x SMs
+    B = args.batch or 4 * torch.cuda.get_device_properties(dev).multi_processor_count
     thetas = theta_sets(circuit.n_params, B, seed=rank)
     table, _ = TR.compile_gates(circuit)
     lo, hi, offs, codes = TR.term_table(terms, n)

@@ -46,7 +46,7 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) { 
   acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
 }
 
-constexpr int NT = 512;
+constexpr int NT = 128;   // threads per CTA: four resident CTAs (theta-sets) per SM hide each other's Jacobi barriers
 constexpr int NW = NT / 32;
 
 template <typename R>
@@ -725,7 +725,7 @@ constexpr int PH_RUN = 1, PH_COMPRESS = 2, PH_VALUES = 4;
 constexpr int PH_TAPE = 8, PH_REPLAY = 16;
 
 template <typename R, int CAP, int PHASE>
-__global__ void __launch_bounds__(NT, 1) tt_kernel(Params p) {
+__global__ void __launch_bounds__(NT, 4) tt_kernel(Params p) {
   using C = typename CT<R>::T;
   constexpr int SLOT = 2 * CAP * CAP;
   constexpr int ESLOT = CAP * CAP;
