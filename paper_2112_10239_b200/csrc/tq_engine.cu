@@ -539,9 +539,17 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
   for (int i = 0; i < st.pass_count; ++i) npb += ch.passes[st.pass_begin + i].bits;
   if (st.pass_count == 0) {
     // every bond bit is introduced by an op here: (alpha, beta) -> tree index is a bijection
-    // onto the last level, so G is read coalesced in its natural order and scattered in smem
+    // onto the last level, so G is read coalesced in its natural order and scattered in smem.
+    // The index separates, idx(al, be) = idx(al, 0) | idx(0, be) (alpha and beta digits land on
+    // disjoint bits): one table per side in the idle U buffer instead of an op walk per pair.
+    int* tal = reinterpret_cast<int*>(ub);
+    int* tbe = tal + st.chi_l;
+    for (int x = tid; x < st.chi_l + st.chi_r; x += TEAM)
+      (x < st.chi_l ? tal[x] : tbe[x - st.chi_l]) =
+          x < st.chi_l ? tree_index(ocode, nops, x, 0) : tree_index(ocode, nops, 0, x - st.chi_l);
+    team_sync<TEAM>();
     for (int pi = tid; pi < np; pi += TEAM) {
-      const int e = tree_index(ocode, nops, pi >> lcr, pi & ((1 << lcr) - 1));
+      const int e = tal[pi >> lcr] | tbe[pi & ((1 << lcr) - 1)];
       ua[2 * e] = gg[pi]; ua[2 * e + 1] = gg[np + pi];
     }
   }
