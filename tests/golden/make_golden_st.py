@@ -133,7 +133,8 @@ def main():
                 rep = run_cli(argv[:1] + ["--circuit", cp, "--ham", hp] + argv[1:])
             cli_runs.append({"argv": ["grad", "--circuit", "mixed", "--ham", "h5", "--engine", "tt"] + extra,
                              "report": rep, "well_posed": w.ok})
-    for n, gates, chi, eps in ((20, 300, 2, 0.0), (40, 2000, 4, 0.0), (30, 900, 3, 0.0), (24, 600, 8, 1e-3)):
+    for n, gates, chi, eps in ((20, 300, 2, 0.0), (40, 2000, 4, 0.0), (30, 900, 3, 0.0), (24, 600, 8, 1e-3),
+                               (500, 5000, 16, 0.0)):   # the last: the reference's `bench tfim` defaults
         argv = ["bench", "tfim", "--n", str(n), "--gates", str(gates), "--chi", str(chi), "--eps", str(eps)]
         with SplitWatch(eps, chi) as w:
             rep = run_cli(argv)
