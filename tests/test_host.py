@@ -150,3 +150,37 @@ def test_reference_objects_compile_directly():
     v, gr = tnsim.grad_expval(c, h, th, engine="tt")
     assert abs(e.real - v) < 1e-12 and np.max(np.abs(g - gr)) < 1e-12
     assert C.structure_key(c) == C.structure_key(c)
+
+
+def test_survey_work_model_matches_section_8d():
+    """bench.py's roofline uses SURVEY.md section 8(d)'s official per-evaluation work; the survey
+    quotes cfg4 F_eval = 1.765e10 flop and B_eval = 1.645e7 bytes, cfg2 1.21e7 / 6.78e4."""
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200 import roofline
+    from paper_2112_10239_b200.workloads import CONFIGS
+
+    for name, f_eval, b_eval in (("cfg4", 1.765e10, 1.645e7), ("cfg2", 1.21e7, 6.78e4)):
+        cfg = CONFIGS[name]
+        terms = C.normalize_terms(cfg.hamiltonian())
+        t1 = sum(1 for _, ops in terms if len(ops) == 1)
+        t2 = sum(1 for _, ops in terms if len(ops) == 2)
+        m = roofline.survey_model(C.compile_chain(cfg.circuit(), terms, "energy", segments=1), t1, t2,
+                                  cfg.layers, cfg.grad)
+        assert abs(m["F_eval"] / f_eval - 1) < 5e-3, (name, m)   # the survey rounds to 3-4 digits
+        assert abs(m["B_eval"] / b_eval - 1) < 5e-3, (name, m)
+
+
+def test_taped_truncation_rule():
+    """The reference's taped path keeps every singular value at eps = 0 (zeros too), so its bond
+    after a split is min(2 chi_l, 2 chi_r): a chi_max below that cuts the tape even when the
+    factored bond fits (autodiff._taped_truncates)."""
+    from paper_2112_10239_b200 import autodiff as AD
+    from paper_2112_10239_b200.maxcut import brickwork_ansatz
+    from paper_2112_10239_b200.workloads import layered_circuit
+
+    bw = brickwork_ansatz(5, 3)                      # factored bond 2, taped bonds reach 4
+    assert not AD._truncating(bw, 0.0, 2) and AD._taped_truncates(bw, 0.0, 2)
+    assert not AD._taped_truncates(bw, 0.0, 4) and not AD._taped_truncates(bw, 0.0, None)
+    assert AD._taped_truncates(bw, 1e-3, None)       # eps > 0 may cut anywhere
+    c = layered_circuit(6, 2)                        # one entangler line: taped bonds stay 2
+    assert not AD._taped_truncates(c, 0.0, 2)
