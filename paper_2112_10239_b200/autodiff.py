@@ -280,11 +280,13 @@ def expval_state(circuit: Circuit, ham: PauliHamiltonian, theta, state, *, want_
     return e.real, grad
 
 
-def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", *, dtype: str = "complex64",
-                       device=None, segments=None):
+def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", eps: float = 0.0, chi_max=None, *,
+                       dtype: str = "complex64", device=None, segments=None):
     """Complex <P> per op-group sharing one state per theta-set (the values of
-    reference taped_expectations, autodiff.py:405-425).  op_groups: dicts {qubit: letter}."""
-    _engine_args(engine, circuit, 0.0, None)
+    reference taped_expectations, autodiff.py:405-425).  op_groups: dicts {qubit: letter}.
+    With a truncation that cuts the reference's tape (eps > 0, or chi_max below its taped bonds)
+    the values come from the taped truncated state, as the reference's do (complex128)."""
+    eps, chi_max = _engine_args(engine, circuit, eps, chi_max)
     arr, single = _check_theta(circuit, theta)
     n = circuit.n_qubits
     from .hamiltonians import PauliTerm
@@ -298,6 +300,12 @@ def expectation_values(circuit: Circuit, theta, op_groups, engine: str = "tt", *
                 raise WireOutOfRange(f"qubit {q} outside 0..{n - 1}")
         terms.append(PauliTerm(1.0, tuple(dict(ops).items())))
     ham_terms = C.normalize_terms(PauliHamiltonian(n, tuple(terms)))
+    if _truncating(circuit, eps, chi_max) or _taped_truncates(circuit, eps, chi_max):
+        from . import truncated as TR
+
+        vals, _ = TR.straight_through(circuit, ham_terms, arr, eps, chi_max, dtype="complex128", device=device,
+                                      want_grad=False)
+        return vals[0] if single else vals
     dev = _device(device)
     dp = E.device_plan(circuit, ham_terms, "values", arr.shape[0], dev, segments, dtype=dtype)
     th = torch.tensor(arr, dtype=E.DTYPES[dtype][1], device=dev)

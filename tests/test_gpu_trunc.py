@@ -195,6 +195,10 @@ def test_truncated_mbe_matches_reference(golden_small):
         np.testing.assert_allclose(grad, r["grad"], atol=1e-9, err_msg=str(kw))
         ev = MC.vertex_expectations(bw, np.array(d["theta"]), graph, **kw)
         np.testing.assert_allclose(ev, r["vertex"], atol=1e-10, err_msg=str(kw))
+        from paper_2112_10239_b200 import autodiff as AD   # taped_expectations with eps / chi_max
+        groups = [{v // 2: "Z" if v % 2 == 0 else "X"} for v in range(10)]
+        vals = AD.expectation_values(bw, np.array(d["theta"]), groups, **kw)
+        np.testing.assert_allclose(vals.real, r["vertex"], atol=1e-10, err_msg=str(kw))
         sol = MC.solve_maxcut(graph, depth=d["depth"], restarts=2, max_iters=6, seed=3, alpha=d["alpha"], **kw)
         assert list(sol.assignment) == r["solve"]["assignment"] and sol.cut_value == r["solve"]["cut"]
         assert sol.restart_index == r["solve"]["restart_index"] and sol.iterations == r["solve"]["iters"]
