@@ -30,6 +30,10 @@
 
 #include "../../include/tq_engine.h"
 
+#ifndef TQ_TEAM32
+#define TQ_TEAM32 512   // threads per chi = 32 team (one CTA); same-box A/B cfg4: 512 3387, 384 3278, 256 3335 evals/s
+#endif
+
 namespace tq {
 
 // ------------------------------------------------------------------ complex helpers
@@ -1842,7 +1846,7 @@ static void set_smem_attr(const void* fn, size_t smem) {
   if (used < 256) { keys[used] = fn; devs[used] = dev; vals[used] = smem; ++used; }
 }
 
-static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : 512); }
+static int team_for_chi(int chi) { return chi <= 8 ? 32 : (chi == 16 ? 128 : TQ_TEAM32); }
 static int chi_bucket(int chi) { int c = 2; while (c < chi) c <<= 1; return c; }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -1970,7 +1974,7 @@ static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rs
 
 template <typename R, int CHI, int FUSED>
 static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
-  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
+  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : TQ_TEAM32);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   const int items = prm.batch * prm.c.n_segments;
   const int grid = (items + TEAMS - 1) / TEAMS;
@@ -2117,7 +2121,7 @@ static tq_status values_impl(const tq_chain* c, int batch, const void* theta, in
 
 template <typename R, int CHI>
 static tq_status launch_inner(InnerParams& ip, cudaStream_t s) {
-  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : 512);
+  constexpr int TEAM = CHI <= 8 ? 32 : (CHI == 16 ? 128 : TQ_TEAM32);
   constexpr int TEAMS = TEAM == 32 ? 4 : 1;
   const size_t csz = 2 * sizeof(R), ms = (size_t)(CHI + 1) * (CHI + 1) * csz;
   size_t off = 0;
