@@ -1205,6 +1205,16 @@ rl_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(3);
     }
+    // CTA teams: the next site's descriptors are resolved by the half of the team the Hermitian
+    // GEMM below leaves idle (rotated thread index), with no barrier in between (disjoint data)
+    int nx2 = -1;
+    if (TEAM >= 128 && has_next) {
+      const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+      nx2 = raw0[0].y;
+      sm.sel(cur ^ 1);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, true, (tid + TEAM / 2) % TEAM, sm.mres, sm.minfo, sm.mps,
+                               sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q - 1, 0));
+    }
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     const bool store = p.store_env && st.env_out >= 0;
     C* envo = env_g + (store ? st.env_out : 0);
@@ -1223,9 +1233,8 @@ rl_sweep(Params p) {
       else gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
     }
     STAGE(5);
-    // resolve the next site's descriptors while the GEMM above is in flight (independent work)
-    int nx2 = -1;
-    if (has_next) {
+    // warp teams: resolve the next site's descriptors after the GEMM (independent work)
+    if (TEAM < 128 && has_next) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].y;
       sm.sel(cur ^ 1);
@@ -1390,6 +1399,16 @@ lr_sweep(Params p) {
       team_sync<TEAM>();
       STAGE(3);
     }
+    int nx2 = -1;
+    if (TEAM >= 128 && has_next) {   // CTA teams: resolved by the half the Hermitian GEMM leaves idle
+      const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+      nx2 = raw0[0].z;
+      sm.sel(cur ^ 1);
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, (tid + TEAM / 2) % TEAM, sm.mres, sm.minfo, sm.mps,
+                               sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q + 1, 1),
+                               wct_as, false, th_pre);
+      sm.sel(cur);
+    }
     // Lam'[bb] = sum_s' AH[s'] BR[bb][s']
     {
       auto la = [&](int, int qq) { return Acur + qq * MS; };
@@ -1398,8 +1417,7 @@ lr_sweep(Params p) {
       if (CHI >= 16 && MODE == 0) gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
       else gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2, la, lb, ls);
     }
-    int nx2 = -1;
-    if (has_next) {   // next site's descriptors, overlapped with this site's GEMMs
+    if (TEAM < 128 && has_next) {   // warp teams: next site's descriptors, overlapped with this site's GEMMs
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].z;
       sm.sel(cur ^ 1);
