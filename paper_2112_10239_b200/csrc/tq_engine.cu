@@ -1400,11 +1400,20 @@ lr_sweep(Params p) {
       STAGE(3);
     }
     int nx2 = -1;
-    if (TEAM >= 128 && has_next) {   // CTA teams: resolved by the half the Hermitian GEMM leaves idle
+    // CTA teams, gradient mode: the Lambda GEMM (Hermitian, half the tiles) and the core-cotangent
+    // GEMM G are independent (LAM vs the dead M slots), so they run side by side on the two halves
+    // of the team, and the next site's descriptors are resolved by the Lambda half's last warp
+    constexpr bool SPLIT = CHI >= 16 && MODE == 0 && TEAM >= 128 && !FUSE;
+    if (pf2 && SPLIT) {   // G reads P(q): landed (with A(q+1))
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      team_sync<TEAM>();
+    }
+    if (TEAM >= 128 && has_next) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].z;
       sm.sel(cur ^ 1);
-      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, (tid + TEAM / 2) % TEAM, sm.mres, sm.minfo, sm.mps,
+      const int rtid = SPLIT ? (tid + TEAM / 2 + 32) % TEAM : (tid + TEAM / 2) % TEAM;
+      stage_blob<R, TEAM, DMW>(raw0, sn, theta_b, coef_b, false, rtid, sm.mres, sm.minfo, sm.mps,
                                sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q + 1, 1),
                                wct_as, false, th_pre);
       sm.sel(cur);
@@ -1414,8 +1423,20 @@ lr_sweep(Params p) {
       auto la = [&](int, int qq) { return Acur + qq * MS; };
       auto lb = [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; };
       auto ls = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); };
-      if (CHI >= 16 && MODE == 0) gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
-      else gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2, la, lb, ls);
+      if constexpr (SPLIT) {
+        if (tid < TEAM / 2) {
+          gemm_group<C, LD, TEAM / 2, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
+        } else {   // G[s'] = sum_bb BR[bb][s'] PIN[bb]  (into the dead M slots)
+          gemm_group<C, LD, TEAM / 2>(tid - TEAM / 2, 2, cl, cr, cr, db,
+              [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
+              [&](int, int qq) { return PIN + qq * MS; },
+              [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+        }
+      } else if (CHI >= 16 && MODE == 0) {
+        gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
+      } else {
+        gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2, la, lb, ls);
+      }
     }
     if (TEAM < 128 && has_next) {   // warp teams: next site's descriptors, overlapped with this site's GEMMs
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
@@ -1426,12 +1447,12 @@ lr_sweep(Params p) {
       sm.sel(cur);
     }
     if constexpr (MODE == 0) {
-      if (pf2) {   // P(q) (and A(q+1)) landed
+      if (pf2 && !SPLIT) {   // P(q) (and A(q+1)) landed
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         team_sync<TEAM>();
       }
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
-      if (!(FUSE && p.L.direct)) gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
+      if (!SPLIT && !(FUSE && p.L.direct)) gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
           [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
           [&](int, int qq) { return PIN + qq * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
