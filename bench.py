@@ -481,7 +481,9 @@ def run_ours(args, cfg):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get("lr_sweep" if kname.startswith("lr") else "rl_sweep")
+            tj = json.load(open(tpath)).get(cfg.name, {})
+            keys = ("lr_sweep", "adj_sweep") if kname.startswith("lr") else ("rl_sweep",)
+            traffic = sum(tj[k] for k in keys) if all(k in tj for k in keys) else None
         except Exception:
             traffic = None
 

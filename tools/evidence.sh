@@ -33,6 +33,10 @@ python bench.py --config cfg4 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null
   cap cfg4 lr_sweep lr_cfg4
   cap cfg4 adj_sweep adj_cfg4
 }
-python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && cap cfg2 rl_sweep rl_cfg2
+python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && {
+  cap cfg2 rl_sweep rl_cfg2
+  cap cfg2 lr_sweep lr_cfg2
+  cap cfg2 adj_sweep adj_cfg2
+}
 python bench.py --config f3 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && cap f3 tt_kernel tt_f3
 ls -la gpurun_out/ev
