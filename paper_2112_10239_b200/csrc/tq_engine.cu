@@ -1110,8 +1110,14 @@ __device__ __forceinline__ const C* wct_row_of(const Params& p, int site, int di
 // ------------------------------------------------------------------ right-to-left sweep
 // Computes the MPO right environments P^{(a)}_k for every cut of the segment's sub-chain,
 // optionally storing them, and the segment's partial energy P^{START}_{lo}.
+#ifndef TQ_RL_MINB
+#define TQ_RL_MINB 4
+#endif
+#ifndef TQ_LR_MINB
+#define TQ_LR_MINB 4
+#endif
 template <typename R, int CHI, int TEAM, int FD>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_RL_MINB : 4) : 1)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
@@ -1253,7 +1259,7 @@ rl_sweep(Params p) {
 // MODE 0: gradient (G + column adjoint); MODE 1: per-term values.  Separate instantiations
 // keep each kernel's code small enough for the instruction cache.
 template <typename R, int CHI, int TEAM, int MODE, int FD>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? 4 : 1)
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_LR_MINB : 4) : 1)
 lr_sweep(Params p) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;

@@ -5,8 +5,9 @@ them for an UNSEGMENTED chain (segments=1), so light-cone halo redundancy never
 inflates ``achieved``:
 
   fold        chi_l*chi_r pairs x ops x 4 cMAC                       (both sweeps)
-  RL          N: 2*Db*chi_l*chi_r^2     P: 2*Da*chi_l^2*chi_r
-  LR          M: 2*Da*chi_l^2*chi_r     Lam: 2*Db*chi_r^2*chi_l     G: 2*Db*chi_l*chi_r^2
+  RL          N: 2*Db*chi_l*chi_r^2     P: 2*Da*chi_l^2*chi_r x h(chi_l)
+  LR          M: 2*Da*chi_l^2*chi_r     Lam: 2*Db*chi_r^2*chi_l x h(chi_r)     G: 2*Db*chi_l*chi_r^2
+              (h = herm_fraction: the Hermitian transfers' upper-tile share, 1 below chi 16)
   adjoint     chi_l*chi_r pairs x ops x 12 cMAC (u and v walks + sigma contraction)
   brackets    2*D*chi_l*chi_r x (edges per channel) cMAC (counted)
 
@@ -19,6 +20,15 @@ from __future__ import annotations
 import numpy as np
 
 
+def herm_fraction(n) -> np.ndarray:
+    """Share of an n x n environment transfer the Hermitian GEMM path computes (n >= 16:
+    4x2 tiles of the upper triangle, tq_engine.cu gemm_group HERM; 72 of 128 tiles at 32)."""
+    n = np.asarray(n, dtype=np.float64)
+    nb, nc = n / 4, n / 2
+    frac = (nb * nc - nb * (nb - 1)) / np.maximum(nb * nc, 1)
+    return np.where(n >= 16, frac, 1.0)
+
+
 def sweep_cmacs(plan) -> dict:
     """cMACs per theta-set: 'rl' right-to-left sweep, 'lr' left-to-right sweep (gradient
     mode with the column adjoint, or values mode with the rho contractions)."""
@@ -28,8 +38,11 @@ def sweep_cmacs(plan) -> dict:
     nops = s["op_count"].astype(np.float64)
     pairs = cl * cr
     fold = pairs * nops * 4
-    rl = 2 * s["rl_db"] * cl * cr * cr + 2 * s["rl_da"] * cl * cl * cr + 2 * s["rl_edge_count"] * cl * cr
-    lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl + 2 * s["lr_db"] * cl * cr * cr
+    # energy mode: the P (RL) and Lambda (LR) transfers are Hermitian, computed on upper tiles
+    hp = herm_fraction(cl) if plan.mode != "values" else 1.0
+    hl = herm_fraction(cr)
+    rl = 2 * s["rl_db"] * cl * cr * cr + 2 * s["rl_da"] * cl * cl * cr * hp + 2 * s["rl_edge_count"] * cl * cr
+    lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl * hl + 2 * s["lr_db"] * cl * cr * cr
           + 2 * s["lr_edge_count"] * cl * cr)
     if plan.mode == "values":
         lr = (2 * s["lr_da"] * cl * cl * cr + 2 * s["lr_db"] * cr * cr * cl + 2 * s["lr_da"] * cl * cr * cr
