@@ -2,7 +2,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void k(double* out, int n) {
-  double acc = 0, acc2 = 0, accd = 0;
+  double acc = 0, acc2 = 0, accd = 0, acc3 = 0, accr = 0, emax = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const float x = (float)((double)i / n * 6.283185307179586 - 3.141592653589793);
     float s, c; sincosf(x * 0.5f, &s, &c);
@@ -11,13 +11,23 @@ __global__ void k(double* out, int n) {
     const float cf = (float)cd, sf = (float)sd;
     acc2 += (double)cf * cf + (double)sf * sf - 1.0;
     accd += ((double)c - cd) * cd + ((double)s - sd) * sd;
+    // sincosf + first-order renormalisation with fused corrections (engine TQ_FAST_SINCOS)
+    const float dd = fmaf(s, s, fmaf(c, c, -1.0f));
+    const float cn = fmaf(c, -0.5f * dd, c), sn = fmaf(s, -0.5f * dd, s);
+    acc3 += (double)cn * cn + (double)sn * sn - 1.0;
+    accr += ((double)cn - cd) * cd + ((double)sn - sd) * sd;
+    emax = fmax(emax, fmax(fabs((double)cn - cd), fabs((double)sn - sd)));
   }
   atomicAdd(out, acc); atomicAdd(out + 1, acc2); atomicAdd(out + 2, accd);
+  atomicAdd(out + 3, acc3); atomicAdd(out + 4, accr);
+  unsigned long long* em = (unsigned long long*)(out + 5);
+  atomicMax(em, (unsigned long long)__double_as_longlong(emax));
 }
 int main() {
-  double* d; cudaMalloc(&d, 24); cudaMemset(d, 0, 24);
+  double* d; cudaMalloc(&d, 48); cudaMemset(d, 0, 48);
   const int n = 1 << 26;
   k<<<1184, 256>>>(d, n);
-  double h[3]; cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+  double h[6]; cudaMemcpy(h, d, 48, cudaMemcpyDeviceToHost);
   printf("sincosf: mean(c^2+s^2-1) = %.3e   fp64-rounded: %.3e   radial err of sincosf = %.3e\n", h[0] / n, h[1] / n, h[2] / n);
+  printf("renormalised sincosf: mean(c^2+s^2-1) = %.3e   radial err = %.3e   max |elem err| = %.3e\n", h[3] / n, h[4] / n, h[5]);
 }
