@@ -263,6 +263,11 @@ class MBEObjective:
         ws = self._scratch(("v", theta.shape[0]), dp, theta.shape[0], True) if dp is self.dp_values else None
         return E.values_raw(dp, theta, dt, ws=ws).real
 
+    def host_evaluator(self, batch: int) -> "_HostEvaluator":
+        """fun(theta [batch, P] numpy) -> (loss [batch], grad [batch, P]) numpy, one captured
+        device round trip per call (the batched form of ``mbe_objective``'s fun)."""
+        return _HostEvaluator(self, batch)
+
     def __call__(self, theta: torch.Tensor):
         r = self.readouts(theta)                                  # [B, V] float64
         t = torch.tanh(self.alpha * r)
@@ -273,6 +278,67 @@ class MBEObjective:
         ws = self._scratch(("e", theta.shape[0]), self.dp_energy, theta.shape[0], False)
         _, grad = E.energy_grad_raw(self.dp_energy, theta, g, True, self.dtype, ws=ws)
         return loss, grad
+
+
+class _HostEvaluator:
+    """Host-buffer serving path of an ``MBEObjective`` for a fixed batch B: pinned theta [B, P]
+    -> device, readout sweeps, tanh loss, gradient sweeps, loss and gradient -> pinned host.
+    The first call runs eagerly; the second captures the whole evaluation as one CUDA graph
+    that every later call replays.  The reference hands one ``fun`` to a thread pool
+    (maxcut.py:309-313): the staging buffers and the captured graph are shared, so one call
+    runs at a time."""
+
+    def __init__(self, obj: "MBEObjective", batch: int):
+        P = obj.circuit.n_params
+        self.obj, self.batch, self.P = obj, int(batch), P
+        self.th_host = torch.empty(batch, P, dtype=torch.float64, pin_memory=True)
+        self.out_host = torch.empty(batch, P + 1, dtype=torch.float64, pin_memory=True)
+        self.th_dev = torch.empty(batch, P, dtype=torch.float64, device=obj.device)
+        self.calls, self.graph = 0, None
+        self.lock = threading.Lock()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.th_host.numel() * 8
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.out_host.numel() * 8
+
+    def _body(self):
+        self.th_dev.copy_(self.th_host, non_blocking=True)
+        loss, grad = self.obj(self.th_dev.to(self.obj.tdt))
+        self.out_host.copy_(torch.cat([loss.reshape(-1, 1).double(), grad.double()], dim=1), non_blocking=True)
+
+    def __call__(self, theta):
+        th = np.asarray(theta, dtype=float)
+        if th.ndim != 2 or th.shape[0] != self.batch:
+            raise SizeMismatch(f"expected theta of shape ({self.batch}, {self.P}), got {th.shape}")
+        if th.shape[1] != self.P:
+            raise ParamCountMismatch(f"expected {self.P} parameters, got {th.shape[1]}")
+        if not np.all(np.isfinite(th)):
+            raise InputError("theta contains non-finite values")
+        with self.lock:
+            self.th_host.numpy()[:] = th
+            dev = self.obj.device
+            if self.graph is None and self.calls >= 1:
+                side = torch.cuda.Stream(device=dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(side):
+                    self._body()
+                torch.cuda.current_stream(dev).wait_stream(side)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                    self._body()
+                self.graph = g
+            self.calls += 1
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._body()
+            torch.cuda.current_stream(dev).synchronize()
+            out = self.out_host.numpy().copy()
+        return out[:, 0], out[:, 1:]
 
 
 def _truncation(engine, circuit, eps, chi_max):
@@ -325,53 +391,12 @@ def mbe_objective(circuit: Circuit, graph: Graph, alpha: float = 1.0, engine: st
     if trunc:
         return _mbe_objective_truncated(circuit, graph, alpha, eps, chi_max, device)
     obj = MBEObjective(circuit, graph, alpha, dtype=dtype, device=device)
-    P = circuit.n_params
-    # Host-buffer serving path: the first call runs eagerly; the second captures the whole
-    # evaluation (pinned theta -> device, readout sweeps, tanh loss, gradient sweeps, loss and
-    # gradient -> pinned host) as one CUDA graph that every later call replays.
-    st = {"calls": 0, "graph": None}
-    th_host = torch.empty(1, P, dtype=torch.float64, pin_memory=True)
-    out_host = torch.empty(1, P + 1, dtype=torch.float64, pin_memory=True)
-    th_dev = torch.empty(1, P, dtype=torch.float64, device=obj.device)
-
-    def body():
-        th_dev.copy_(th_host, non_blocking=True)
-        loss, grad = obj(th_dev.to(obj.tdt))
-        out_host.copy_(torch.cat([loss.reshape(1, 1).double(), grad.double()], dim=1), non_blocking=True)
-
-    lock = threading.Lock()
+    call = obj.host_evaluator(1)
 
     def fun(theta):
         th = np.asarray(theta, dtype=float).reshape(-1)
-        if th.shape[0] != P:
-            raise ParamCountMismatch(f"expected {P} parameters, got {th.shape[0]}")
-        if not np.all(np.isfinite(th)):
-            raise InputError("theta contains non-finite values")
-        # the reference hands one `fun` to a thread pool (maxcut.py:309-313): the staging buffers,
-        # the call counter and the captured graph are shared, so one call runs at a time
-        with lock:
-            return _call(th)
-
-    def _call(th):
-        th_host.numpy()[0] = th
-        if st["graph"] is None and st["calls"] >= 1:
-            side = torch.cuda.Stream(device=obj.device)
-            side.wait_stream(torch.cuda.current_stream(obj.device))
-            with torch.cuda.stream(side):
-                body()
-            torch.cuda.current_stream(obj.device).wait_stream(side)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="relaxed"):
-                body()
-            st["graph"] = g
-        st["calls"] += 1
-        if st["graph"] is not None:
-            st["graph"].replay()
-        else:
-            body()
-        torch.cuda.current_stream(obj.device).synchronize()
-        out = out_host.numpy()[0].copy()
-        return float(out[0]), out[1:]
+        loss, grad = call(th.reshape(1, -1))
+        return float(loss[0]), grad[0]
 
     return fun
 

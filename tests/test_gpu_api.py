@@ -268,3 +268,29 @@ def test_mbe_objective_captured_calls_track_inputs(golden_small):
         fun(np.zeros(c.n_params + 1))
     with pytest.raises(InputError):
         fun(np.full(c.n_params, np.nan))
+
+
+def test_mbe_host_evaluator_batched_matches_per_restart(golden_small):
+    """MBEObjective.host_evaluator(B): B restarts per captured host round trip (the cfg3 bench
+    e2e path) equal B single-restart calls of the reference-shaped mbe_objective fun."""
+    from paper_2112_10239_b200.errors import ParamCountMismatch, SizeMismatch
+
+    d = golden_small["mbe10"]
+    g = MC.Graph(10, tuple(tuple(e) for e in d["edges"]))
+    c = MC.brickwork_ansatz(5, d["depth"])
+    fun = MC.mbe_objective(c, g, alpha=d["alpha"], dtype="complex128")
+    obj = MC.MBEObjective(c, g, d["alpha"], dtype="complex128", device="cuda:0", batch=3)
+    hev = obj.host_evaluator(3)
+    rng = np.random.default_rng(5)
+    for _ in range(3):   # eager, capture, replay
+        th = rng.uniform(-np.pi, np.pi, (3, c.n_params))
+        loss, grad = hev(th)
+        for r in range(3):
+            l1, g1 = fun(th[r])
+            assert abs(loss[r] - l1) < 1e-10
+            np.testing.assert_allclose(grad[r], g1, atol=1e-10)
+    assert hev.h2d_bytes == 3 * c.n_params * 8 and hev.d2h_bytes == 3 * (c.n_params + 1) * 8
+    with pytest.raises(SizeMismatch):
+        hev(np.zeros((2, c.n_params)))
+    with pytest.raises(ParamCountMismatch):
+        hev(np.zeros((3, c.n_params + 1)))
