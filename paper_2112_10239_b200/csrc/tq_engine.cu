@@ -75,6 +75,7 @@ struct Layout {          // byte offsets inside one team's shared-memory slab (h
   int32_t a2;            // second folded-core buffer (direct path)
   int32_t wc;            // fused path: per-site channel-pair 2x2 bracket matrices + nonzero mask
   int32_t lrpf;          // chi >= 16 gradient LR sweep: A (ping-pong A / A2) and P cp.async-prefetched
+  int32_t rlpre;         // chi >= 16 energy RL sweep: the next site is folded into A2 (ping-pong) during P
   int32_t team_bytes;
 };
 
@@ -124,6 +125,14 @@ __device__ unsigned long long g_stage_cycles[2][16];
 // Team barrier: a warp team syncs with __syncwarp, a CTA team with __syncthreads.
 template <int TEAM> __device__ __forceinline__ void team_sync() {
   if (TEAM == 32) __syncwarp(); else __syncthreads();
+}
+
+// Barrier 1 over the upper N threads of a CTA (the half the split stages hand independent work)
+template <int N> __device__ __forceinline__ void upper_sync() {
+#ifdef TQ_DEBUG_RACE
+  tq_dbg_delay();
+#endif
+  asm volatile("bar.sync 1, %0;" :: "r"(N) : "memory");
 }
 
 // Pauli op element <s'|O|s>: for op in {I,X,Y,Z} the only nonzero s for a given s' and its factor.
@@ -465,6 +474,44 @@ __device__ void fold_site2(const tq_chain& ch, const tq_site& st, int tid, const
     if (hb) {
       if (st.pass_count && !pass_ok(ch, st, alb, beb)) { b0 = z; b1 = z; }
       A[alb * LD + beb] = b0; A[LD * LD + alb * LD + beb] = b1;
+    }
+  }
+}
+
+// Four pairs per thread in lockstep: the RL sweep's next-site fold on half a CTA (1024 pairs on
+// 256 threads) while the other half runs the Hermitian P GEMM.
+template <typename R, int LD, int TEAM>
+__device__ void fold_site4(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                           const int* ocode, typename CT<R>::T* A, int lcr) {
+  using C = typename CT<R>::T;
+  const int npair = st.chi_l * st.chi_r;
+  const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
+  const C z = cmk<C>(R(0), R(0));
+  for (int p0 = tid; p0 < npair; p0 += 4 * TEAM) {
+    int al[4], be[4];
+    C v0[4], v1[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int pp = p0 + k * TEAM < npair ? p0 + k * TEAM : p0;
+      al[k] = pp >> lcr; be[k] = pp & (st.chi_r - 1);
+      v0[k] = i0; v1[k] = i1;
+    }
+    for (int oi = 0; oi < st.op_count; ++oi) {
+      const int c = ocode[oi];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al[k], be[k]));
+        const C m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3];
+        C n0 = cmul(m0, v0[k]), n1 = cmul(m2, v0[k]);
+        cfma(n0, m1, v1[k]); cfma(n1, m3, v1[k]);
+        v0[k] = n0; v1[k] = n1;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (p0 + k * TEAM >= npair) break;
+      if (st.pass_count && !pass_ok(ch, st, al[k], be[k])) { v0[k] = z; v1[k] = z; }
+      A[al[k] * LD + be[k]] = v0[k]; A[LD * LD + al[k] * LD + be[k]] = v1[k];
     }
   }
 }
@@ -1168,6 +1215,11 @@ rl_sweep(Params p) {
     if (nx >= 0) blob_prefetch(raw0, blob + nx, p.c.blob_max, tid, TEAM);
   }
   int cur = 0;
+  // CTA teams in energy mode: the folded core ping-pongs between A and A2, and the next site is
+  // folded (and stored) by the half of the CTA the Hermitian P GEMM leaves idle
+  C* Acur = sm.A;
+  C* Anext = reinterpret_cast<C*>(smem_raw + (size_t)team * p.L.team_bytes + p.L.a2);
+  bool folded = false;
   for (int q = seg.site_count - 1; q >= 0; --q, cur ^= 1) {
     team_sync<TEAM>();
     sm.sel(cur);
@@ -1177,30 +1229,32 @@ rl_sweep(Params p) {
     const int lcl = 31 - __clz(cl), lcr = 31 - __clz(cr);
     const int db = st.rl_db, da = st.rl_da;
     STAGE(0);
-    // per-pair column walks: the digit-tree fold (levels in the dead N/BR slots) was measured
-    // slower at chi = 32 (11.7k vs 7.7k cycles per site: 20 team barriers over small levels)
-    if constexpr (TEAM >= 128) fold_site2<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, lcr);
-    else fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, sm.A, nullptr, lcr);
-    team_sync<TEAM>();
-    if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
-      C* ag = env_g + st.a_off;
-      const int np = cl * cr;
-      for (int e = tid; e < 2 * np; e += TEAM) {
-        const int sidx = e >= np, r = e - sidx * np;
-        ag[e] = sm.A[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))];
+    if (!folded) {
+      // per-pair column walks: the digit-tree fold (levels in the dead N/BR slots) was measured
+      // slower at chi = 32 (11.7k vs 7.7k cycles per site: 20 team barriers over small levels)
+      if constexpr (TEAM >= 128) fold_site2<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, Acur, lcr);
+      else fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, Acur, nullptr, lcr);
+      team_sync<TEAM>();
+      if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
+        C* ag = env_g + st.a_off;
+        const int np = cl * cr;
+        for (int e = tid; e < 2 * np; e += TEAM) {
+          const int sidx = e >= np, r = e - sidx * np;
+          ag[e] = Acur[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))];
+        }
       }
     }
     STAGE(1);
     if constexpr (FUSE) {
       // fused: N[b][s] = A[s] P[b] kept in registers, brackets written directly
-      product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, sm.A, PIN, WC, sm.BR);
+      product_bracket<R, LD, TEAM, FDM, FRT>(tid, true, db, da, cl, cr, lcl, lcr, Acur, PIN, WC, sm.BR);
       blob_wait();
       team_sync<TEAM>();
       STAGE(2);
     } else {
       // N[b][s] = A[s] * P[b]
       gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
-            [&](int t, int) { return sm.A + (t & 1) * MS; },
+            [&](int t, int) { return Acur + (t & 1) * MS; },
             [&](int t, int) { return PIN + (t >> 1) * MS; },
             [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
@@ -1212,8 +1266,54 @@ rl_sweep(Params p) {
       STAGE(3);
     }
     // CTA teams: the next site's descriptors are resolved by the half of the team the Hermitian
-    // GEMM below leaves idle (rotated thread index), with no barrier in between (disjoint data)
+    // GEMM below leaves idle (rotated thread index), with no barrier in between (disjoint data).
+    // With the A2 buffer (energy mode, descriptors staged without a team barrier) that half also
+    // folds the next site and stores its core while the other half runs the GEMM.
     int nx2 = -1;
+    const bool pre = TEAM >= 128 && p.L.rlpre && has_next && p.mode == 0 &&
+                     (DMW == 0 || wct_row(p, seg.site_begin + q - 1, 0) != nullptr);
+    const bool store = p.store_env && st.env_out >= 0;
+    C* envo = env_g + (store ? st.env_out : 0);
+    auto pa = [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; };
+    auto pb = [&](int, int qq) { return Acur + qq * MS; };
+    auto ps = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
+      store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
+      if (store) {
+        C* h = envo + ((size_t)t << (2 * lcl)) + (i0 << lcl) + j;
+        h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
+      }
+    };
+    if constexpr (TEAM >= 128) if (pre) {
+      nx2 = raw0[0].y;
+      if (tid >= TEAM / 2) {
+        const int ut = tid - TEAM / 2;
+        const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
+        sm.sel(cur ^ 1);
+        stage_blob<R, TEAM / 2, DMW>(raw0, sn, theta_b, coef_b, true, ut, sm.mres, sm.minfo, sm.mps, sm.ocode,
+                                     sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q - 1, 0));
+        upper_sync<TEAM / 2>();
+        const int ncr = sn.chi_r, nlcr = 31 - __clz(ncr);
+        fold_site4<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
+        if (p.store_env) {
+          upper_sync<TEAM / 2>();
+          C* ag = env_g + sn.a_off;
+          const int np = sn.chi_l * ncr;
+          for (int e = ut; e < 2 * np; e += TEAM / 2) {
+            const int sidx = e >= np, r = e - sidx * np;
+            ag[e] = Anext[sidx * MS + (r >> nlcr) * LD + (r & (ncr - 1))];
+          }
+        }
+      } else {
+        gemm_group<C, LD, TEAM / 2, false, true, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+      }
+      team_sync<TEAM>();
+      STAGE(4);
+      if (nx2 >= 0) blob_prefetch(raw0, blob + nx2, p.c.blob_max, tid, TEAM);
+      C* t = Acur; Acur = Anext; Anext = t;
+      folded = true;
+      continue;
+    }
+    folded = false;
     if (TEAM >= 128 && has_next) {
       const tq_site sn = *reinterpret_cast<const tq_site*>(raw0 + 1);
       nx2 = raw0[0].y;
@@ -1222,18 +1322,7 @@ rl_sweep(Params p) {
                                sm.ocode, sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q - 1, 0));
     }
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
-    const bool store = p.store_env && st.env_out >= 0;
-    C* envo = env_g + (store ? st.env_out : 0);
     {
-      auto pa = [&](int t, int qq) { return sm.BR + (t * 2 + qq) * MS; };
-      auto pb = [&](int, int qq) { return sm.A + qq * MS; };
-      auto ps = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
-        store_rows<C, LD>(PIN + t * MS + i0 * LD + j, rt, a0, a1, a2, a3);
-        if (store) {
-          C* h = envo + ((size_t)t << (2 * lcl)) + (i0 << lcl) + j;
-          h[0] = a0; if (rt > 1) h[cl] = a1; if (rt > 2) { h[2 * cl] = a2; h[3 * cl] = a3; }
-        }
-      };
       // the environments of the energy / gradient MPO are Hermitian (real coefficients): half the work
       if (CHI >= 16 && p.mode == 0) gemm_group<C, LD, TEAM, false, true, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
       else gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
@@ -1915,8 +2004,9 @@ static Layout make_layout(const tq_chain* c, int chi, int team, size_t rsz, bool
   L.pin = (int32_t)off;
   if (lr) off += (size_t)D * ms;                      // direct path: P dense, prefetched
   L.lrpf = (lr && mode == 0 && chi >= 16) ? 1 : 0;
+  L.rlpre = (!lr && mode == 0 && chi >= 16 && team >= 128) ? 1 : 0;
   L.a2 = (int32_t)off;
-  if (L.direct || L.lrpf) off += 2 * ms;
+  if (L.direct || L.lrpf || L.rlpre) off += 2 * ms;
   off = align_up(off, 16);
   L.wc = (int32_t)off;
   if (fused || wbr) { const int dm = D <= 3 ? 3 : 4; off += align_up((size_t)dm * dm * 4 * csz + 16, 16); }
