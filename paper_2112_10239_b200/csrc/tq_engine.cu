@@ -530,32 +530,33 @@ __device__ void fold_site4(const tq_chain& ch, const tq_site& st, int tid, const
 // fit on an SM.
 template <typename R, int TEAM>
 __device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
-                              typename CT<R>::T* levt, typename CT<R>::T* buf0, typename CT<R>::T* buf1,
-                              int* tbase) {
+                              typename CT<R>::T* levt, typename CT<R>::T* scratch, int* tbase) {
   using C = typename CT<R>::T;
   const C i0 = cmk<C>(R(st.init[0]), R(st.init[1])), i1 = cmk<C>(R(st.init[2]), R(st.init[3]));
   const C* src = nullptr;   // null: the initial vector
   int tb = 0;
   for (int oi = 0; oi < st.op_count; ++oi) {
     const int c = ocode[oi];
-    const int toff = oc_toff(c), nn = 1 << (toff + oc_bits(c));
+    const int toff = oc_toff(c), nd = 1 << oc_bits(c), npv = 1 << toff;
     C* dst;
     if (oc_tidx(c) >= 0) {
       dst = levt + 2 * tb;
       if (tid == 0) tbase[oi] = tb;
-      tb += nn;
+      tb += npv * nd;
     } else {
-      dst = src == buf0 ? buf1 : buf0;   // never the level being read
+      dst = scratch;   // possibly the level being read: one thread owns idx and all its children
     }
     const C* Mb = mres + 4 * oc_lmat(c);
-    for (int e = tid; e < nn; e += TEAM) {
-      const int idx = e & ((1 << toff) - 1);
-      const C* M = Mb + 4 * (e >> toff);
+    for (int idx = tid; idx < npv; idx += TEAM) {
       const C v0 = src ? src[2 * idx] : i0;
       const C v1 = src ? src[2 * idx + 1] : i1;
-      C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
-      C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
-      dst[2 * e] = n0; dst[2 * e + 1] = n1;
+      for (int d = 0; d < nd; ++d) {
+        const C* M = Mb + 4 * d;
+        C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
+        C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
+        const int e = idx + (d << toff);
+        dst[2 * e] = n0; dst[2 * e + 1] = n1;
+      }
     }
     team_sync<TEAM>();
     src = dst;
@@ -578,8 +579,7 @@ __device__ __forceinline__ int tree_index(const int* ocode, int nops, int al, in
 template <typename R, int TEAM>
 __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
                               const int* minfo, const int* ocode, const typename CT<R>::T* levt, const int* tbase,
-                              typename CT<R>::T* ua, typename CT<R>::T* ub, const typename CT<R>::T* gg, int lcr,
-                              R* contrib) {
+                              typename CT<R>::T* ua, int* tal, const typename CT<R>::T* gg, int lcr, R* contrib) {
   using C = typename CT<R>::T;
   const int nops = st.op_count;
   if (nops == 0) return;
@@ -592,8 +592,7 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
     // every bond bit is introduced by an op here: (alpha, beta) -> tree index is a bijection
     // onto the last level, so G is read coalesced in its natural order and scattered in smem.
     // The index separates, idx(al, be) = idx(al, 0) | idx(0, be) (alpha and beta digits land on
-    // disjoint bits): one table per side in the idle U buffer instead of an op walk per pair.
-    int* tal = reinterpret_cast<int*>(ub);
+    // disjoint bits): one table per side instead of an op walk per pair.
     int* tbe = tal + st.chi_l;
     for (int x = tid; x < st.chi_l + st.chi_r; x += TEAM)
       (x < st.chi_l ? tal[x] : tbe[x - st.chi_l]) =
@@ -655,6 +654,7 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
       if ((tid & 31) == 0) contrib[tix * (TEAM / 32) + (tid >> 5)] += acc;   // per-warp partials
     }
     if (oi > 0) {
+      // in place: entry idx is read (with its children idx | d << toff) and written by one thread
       const int npv = 1 << toff;
       for (int idx = tid; idx < npv; idx += TEAM) {
         C w0 = cmk<C>(R(0), R(0)), w1 = w0;
@@ -664,9 +664,8 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
           cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
           cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
         }
-        ub[2 * idx] = w0; ub[2 * idx + 1] = w1;
+        ua[2 * idx] = w0; ua[2 * idx + 1] = w1;
       }
-      C* t = ua; ua = ub; ub = t;
     }
   }
   team_sync<TEAM>();
@@ -1521,11 +1520,16 @@ lr_sweep(Params p) {
       if constexpr (SPLIT) {
         if (tid < TEAM / 2) {
           gemm_group<C, LD, TEAM / 2, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
-        } else {   // G[s'] = sum_bb BR[bb][s'] PIN[bb]  (into the dead M slots)
+        } else {   // G[s'] = sum_bb BR[bb][s'] PIN[bb], straight from the epilogue to HBM (dense [2][cl][cr])
+          C* const gg = env_g_w + st.g_off;
+          const int np = cl * cr;
           gemm_group<C, LD, TEAM / 2>(tid - TEAM / 2, 2, cl, cr, cr, db,
               [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
               [&](int, int qq) { return PIN + qq * MS; },
-              [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
+              [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
+                C* h = gg + (size_t)t * np + i0 * cr + j;
+                h[0] = a0; if (rt > 1) h[cr] = a1; if (rt > 2) { h[2 * cr] = a2; h[3 * cr] = a3; }
+              });
         }
       } else if (CHI >= 16 && MODE == 0) {
         gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
@@ -1574,7 +1578,7 @@ lr_sweep(Params p) {
           }
           gg[tid] = g0; gg[np + tid] = g1;
         }
-      } else {
+      } else if (!SPLIT) {
         for (int e = tid; e < 2 * np; e += TEAM) {
           const int sidx = e >= np, r = e - sidx * np;
           gg[e] = G[sidx * MS + (r >> lcr) * LD + (r & (cr - 1))];
@@ -1657,7 +1661,8 @@ lr_sweep(Params p) {
 // the left-to-right sweep's sequential critical path.
 struct AdjLayout {
   int32_t g, mres, minfo, mps, ocode, ogidx, obase, sbuf, raw, lev, ubuf, contrib, team_bytes, tree;
-  int32_t ubuf_vec;   // 2-vectors per U / scratch buffer of the compact digit tree
+  int32_t ubuf_vec;   // 2-vectors in the compact digit tree's scratch / U buffer
+  int32_t utab;       // the leaf-index tables (alpha and beta sides) of the adjoint's gather
 };
 
 // Min resident 128-thread adjoint CTAs per SM (team-of-32 path).  6 measured best
@@ -1666,8 +1671,11 @@ struct AdjLayout {
 #ifndef TQ_ADJ_MINB
 #define TQ_ADJ_MINB 6
 #endif
+#ifndef TQ_ADJ128_MINB
+#define TQ_ADJ128_MINB 4
+#endif
 template <typename R, int CHI, int TEAM>
-__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : (TEAM == 128 ? 4 : 1))
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : (TEAM == 128 ? (sizeof(R) == 4 ? TQ_ADJ128_MINB : 4) : 1))
 adj_sweep(Params p, AdjLayout A) {
   using C = typename CT<R>::T;
   constexpr int LD = CHI + 1;
@@ -1746,11 +1754,11 @@ adj_sweep(Params p, AdjLayout A) {
   if constexpr (CHI >= 16) {
     if (A.tree) {
       C* lev = reinterpret_cast<C*>(base + A.lev);
-      C* u0 = reinterpret_cast<C*>(base + A.ubuf);
-      C* u1 = u0 + 2 * (A.ubuf_vec);
+      C* u0 = reinterpret_cast<C*>(base + A.ubuf);       // forward scratch, then U (in place)
+      int* tal = reinterpret_cast<int*>(base + A.utab);
       int* tbase = obase;   // host tbase offsets are for the full tree; the compact ones go here
-      ctree_forward<R, TEAM>(st, tid, mres, ocode, lev, u0, u1, tbase);
-      ctree_adjoint<R, TEAM>(p.c, st, tid, mres, minfo, ocode, lev, tbase, u0, u1, gg, lcr, contrib);
+      ctree_forward<R, TEAM>(st, tid, mres, ocode, lev, u0, tbase);
+      ctree_adjoint<R, TEAM>(p.c, st, tid, mres, minfo, ocode, lev, tbase, u0, tal, gg, lcr, contrib);
     }
   }
   const bool one_pair = np <= TEAM;
@@ -2092,14 +2100,16 @@ static AdjLayout make_adj_layout(const tq_chain* c, int chi, int team, size_t rs
   A.tree = 0;
   A.ubuf_vec = chi * chi;
   if (chi >= 16) {
-    // compact digit tree: kept (trainable) levels + two buffers of chi^2 2-vectors; G is read
-    // from HBM, so no G slab
+    // compact digit tree: kept (trainable) levels + one buffer of chi^2 2-vectors (forward
+    // scratch, then U; both walks run in place) + the gather's leaf tables; G is read from HBM,
+    // so no G slab
     const int kept = c->max_ttree > 0 ? c->max_ttree : (c->max_tree > 0 ? c->max_tree : 1);
     const size_t lev = (size_t)kept * 2 * csz;
-    const size_t ub = (size_t)2 * A.ubuf_vec * 2 * csz;
+    const size_t ub = (size_t)A.ubuf_vec * 2 * csz;
+    const size_t tab = (size_t)2 * chi * 4;
     const size_t ctb = (size_t)ntr * (team / 32) * rsz;
-    if (align_up(off + lev + ub + ctb + 64, 128) <= budget) {
-      A.tree = 1; A.lev = take(lev); A.ubuf = take(ub); A.contrib = take(ctb);
+    if (align_up(off + lev + ub + tab + ctb + 96, 128) <= budget) {
+      A.tree = 1; A.lev = take(lev); A.ubuf = take(ub); A.utab = take(tab); A.contrib = take(ctb);
     }
   }
   if (!A.tree) { A.g = take(2 * ms); A.contrib = take((size_t)ntr * team * rsz); }
