@@ -829,8 +829,8 @@ def run_f3(args):
     dev = torch.device("cuda", local)
     circuit, terms = f3_problem()
     n, T = circuit.n_qubits, len(terms)
-    # four 128-thread CTAs (theta-sets) resident per SM (csrc/tq_trunc.cu NT): one wave of 4 x SMs
-    B = args.batch or 4 * torch.cuda.get_device_properties(dev).multi_processor_count
+    # six 128-thread CTAs (theta-sets) resident per SM (csrc/tq_trunc.cu NT, TQT_MINB): one wave
+    B = args.batch or 6 * torch.cuda.get_device_properties(dev).multi_processor_count
     thetas = theta_sets(circuit.n_params, B, seed=rank)
     table, _ = TR.compile_gates(circuit)
     lo, hi, offs, codes = TR.term_table(terms, n)

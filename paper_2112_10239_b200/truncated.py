@@ -628,7 +628,7 @@ def straight_through(circuit: Circuit, terms, theta, eps: float = 0.0, chi_max=N
         # within a 16 GB workspace budget (HBM is 180 GB; a row at n=500, cap 16 takes ~8 MB)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         per_row = int(lib.tq_tt_workspace_bytes(n, 1, cap, code))
-        rows_per_launch = int(max(sms, min(4 * sms, (16 << 30) // max(per_row, 1))))
+        rows_per_launch = int(max(sms, min(6 * sms, (16 << 30) // max(per_row, 1))))
     e = np.zeros(len(rows))
     for c0 in range(0, len(rows), rows_per_launch):
         chunk = rows[c0:c0 + rows_per_launch]
