@@ -134,6 +134,16 @@ template <int N> __device__ __forceinline__ void upper_sync() {
 #endif
   asm volatile("bar.sync 1, %0;" :: "r"(N) : "memory");
 }
+// The same barrier, also returning the AND of every participating thread's predicate
+template <int N> __device__ __forceinline__ bool upper_sync_and(bool pred) {
+#ifdef TQ_DEBUG_RACE
+  tq_dbg_delay();
+#endif
+  unsigned out;
+  asm volatile("{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.and.pred q, 1, %2, p;\n selp.u32 %0, 1, 0, q;\n}"
+               : "=r"(out) : "r"((unsigned)pred), "r"(N) : "memory");
+  return out != 0;
+}
 
 // Pauli op element <s'|O|s>: for op in {I,X,Y,Z} the only nonzero s for a given s' and its factor.
 template <typename C> __device__ __forceinline__ int pauli_src(int op, int sp) { return (op == 1 || op == 2) ? 1 - sp : sp; }
@@ -512,6 +522,46 @@ __device__ void fold_site4(const tq_chain& ch, const tq_site& st, int tid, const
       if (p0 + k * TEAM >= npair) break;
       if (st.pass_count && !pass_ok(ch, st, al[k], be[k])) { v0[k] = z; v1[k] = z; }
       A[al[k] * LD + be[k]] = v0[k]; A[LD * LD + al[k] * LD + be[k]] = v1[k];
+    }
+  }
+}
+
+// fold_site4 for a real column (real initial vector, every factor real: ry rotations and real
+// constant factors such as the CZ / CNOT projector splits): the walk runs on real 2-vectors,
+// 4 FMA per op and pair instead of 16, and A gets zero imaginary parts.  Bit-identical to the
+// complex walk (every imaginary term it would add is an exact zero).
+template <typename R, int LD, int TEAM>
+__device__ void fold_site4r(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                            const int* ocode, typename CT<R>::T* A, int lcr) {
+  using C = typename CT<R>::T;
+  const int npair = st.chi_l * st.chi_r;
+  const R i0 = R(st.init[0]), i1 = R(st.init[2]);
+  for (int p0 = tid; p0 < npair; p0 += 4 * TEAM) {
+    int al[4], be[4];
+    R v0[4], v1[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int pp = p0 + k * TEAM < npair ? p0 + k * TEAM : p0;
+      al[k] = pp >> lcr; be[k] = pp & (st.chi_r - 1);
+      v0[k] = i0; v1[k] = i1;
+    }
+    for (int oi = 0; oi < st.op_count; ++oi) {
+      const int c = ocode[oi];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al[k], be[k]));
+        const R m0 = M[0].x, m1 = M[1].x, m2 = M[2].x, m3 = M[3].x;
+        const R n0 = fma(m1, v1[k], m0 * v0[k]);
+        const R n1 = fma(m3, v1[k], m2 * v0[k]);
+        v0[k] = n0; v1[k] = n1;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (p0 + k * TEAM >= npair) break;
+      R a0 = v0[k], a1 = v1[k];
+      if (st.pass_count && !pass_ok(ch, st, al[k], be[k])) { a0 = R(0); a1 = R(0); }
+      A[al[k] * LD + be[k]] = cmk<C>(a0, R(0)); A[LD * LD + al[k] * LD + be[k]] = cmk<C>(a1, R(0));
     }
   }
 }
@@ -1290,9 +1340,19 @@ rl_sweep(Params p) {
         sm.sel(cur ^ 1);
         stage_blob<R, TEAM / 2, DMW>(raw0, sn, theta_b, coef_b, true, ut, sm.mres, sm.minfo, sm.mps, sm.ocode,
                                      sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q - 1, 0));
-        upper_sync<TEAM / 2>();
+        // is the column real?  each thread checks the factors it just resolved (ry and real
+        // constants are real; rx / rz or a complex constant are not); the barrier ANDs them
+        bool real = sn.init[1] == 0.0 && sn.init[3] == 0.0;
+        for (int e = ut; e < sn.lmat_count; e += TEAM / 2) {
+          const int kind = sm.minfo[e] & 0xff;
+          const C* m = sm.mres + 4 * e;
+          if (kind == 1 || kind == 3 || (kind == 0 && (m[0].y != R(0) || m[1].y != R(0) || m[2].y != R(0) || m[3].y != R(0))))
+            real = false;
+        }
+        real = upper_sync_and<TEAM / 2>(real);
         const int ncr = sn.chi_r, nlcr = 31 - __clz(ncr);
-        fold_site4<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
+        if (real) fold_site4r<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
+        else fold_site4<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
         if (p.store_env) {
           upper_sync<TEAM / 2>();
           C* ag = env_g + sn.a_off;
