@@ -449,6 +449,45 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
   }
 }
 
+// fold_site (no AH) for a real column, as fold_site4r: real 2-vectors, 4 FMA per op, bit-identical.
+template <typename R, int LD, int TEAM>
+__device__ void fold_site_real(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
+                               const int* ocode, typename CT<R>::T* A, int lcr) {
+  using C = typename CT<R>::T;
+  const int npair = st.chi_l * st.chi_r;
+  for (int pi = tid; pi < npair; pi += TEAM) {
+    const int al = pi >> lcr, be = pi & (st.chi_r - 1);
+    R v0 = R(st.init[0]), v1 = R(st.init[2]);
+    if (st.pass_count && !pass_ok(ch, st, al, be)) { v0 = R(0); v1 = R(0); }
+    else {
+#pragma unroll 4
+      for (int oi = 0; oi < st.op_count; ++oi) {
+        const int c = ocode[oi];
+        const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al, be));
+        const R n0 = fma(M[1].x, v1, M[0].x * v0);
+        const R n1 = fma(M[3].x, v1, M[2].x * v0);
+        v0 = n0; v1 = n1;
+      }
+    }
+    A[al * LD + be] = cmk<C>(v0, R(0)); A[LD * LD + al * LD + be] = cmk<C>(v1, R(0));
+  }
+}
+
+// Is the column real?  Checks the resolved factors with indices tid, tid + STRIDE, ... (ry and
+// real constants are real; rx / rz and complex constants are not) and the input vector; the
+// caller ANDs the result over the threads that cover every factor.
+template <typename R, int STRIDE>
+__device__ __forceinline__ bool column_real(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* minfo) {
+  using C = typename CT<R>::T;
+  bool real = st.init[1] == 0.0 && st.init[3] == 0.0;
+  for (int e = tid; e < st.lmat_count; e += STRIDE) {
+    const int kind = minfo[e] & 0xff;
+    const C* m = mres + 4 * e;
+    if (kind == 1 || kind == 3 || (kind == 0 && (m[0].y != R(0) || m[1].y != R(0) || m[2].y != R(0) || m[3].y != R(0))))
+      real = false;
+  }
+  return real;
+}
 
 // The same fold with two pairs per thread walked in lockstep (CTA teams, chi >= 16: 1024 pairs
 // on 512 threads).  The column is a chain of dependent 2x2 matvecs; interleaving two
@@ -1282,6 +1321,8 @@ rl_sweep(Params p) {
       // per-pair column walks: the digit-tree fold (levels in the dead N/BR slots) was measured
       // slower at chi = 32 (11.7k vs 7.7k cycles per site: 20 team barriers over small levels)
       if constexpr (TEAM >= 128) fold_site2<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, Acur, lcr);
+      else if (__all_sync(0xffffffffu, column_real<R, TEAM>(st, tid, sm.mres, sm.minfo)))
+        fold_site_real<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, Acur, lcr);
       else fold_site<R, LD, TEAM>(p.c, st, tid, sm.mres, sm.ocode, Acur, nullptr, lcr);
       team_sync<TEAM>();
       if (p.store_env) {   // the left-to-right sweep reloads the folded core instead of refolding
@@ -1342,14 +1383,7 @@ rl_sweep(Params p) {
                                      sm.ogidx, sm.obase, sm.sedge, sm.sbuf, WC, wct_row(p, seg.site_begin + q - 1, 0));
         // is the column real?  each thread checks the factors it just resolved (ry and real
         // constants are real; rx / rz or a complex constant are not); the barrier ANDs them
-        bool real = sn.init[1] == 0.0 && sn.init[3] == 0.0;
-        for (int e = ut; e < sn.lmat_count; e += TEAM / 2) {
-          const int kind = sm.minfo[e] & 0xff;
-          const C* m = sm.mres + 4 * e;
-          if (kind == 1 || kind == 3 || (kind == 0 && (m[0].y != R(0) || m[1].y != R(0) || m[2].y != R(0) || m[3].y != R(0))))
-            real = false;
-        }
-        real = upper_sync_and<TEAM / 2>(real);
+        const bool real = upper_sync_and<TEAM / 2>(column_real<R, TEAM / 2>(sn, ut, sm.mres, sm.minfo));
         const int ncr = sn.chi_r, nlcr = 31 - __clz(ncr);
         if (real) fold_site4r<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
         else fold_site4<R, LD, TEAM / 2>(p.c, sn, ut, sm.mres, sm.ocode, Anext, nlcr);
