@@ -122,6 +122,11 @@ typedef struct {
   int32_t max_pairs;            /* largest chi_l*chi_r of any site */
   int32_t max_ttree;            /* largest sum of trainable-op digit-tree levels (entries) of any column;
                                    0 = unknown (the adjoint then sizes its kept levels by max_tree) */
+  int32_t real_path;            /* 1: every factor matrix, input vector and MPO edge is real (ry
+                                   rotations, real constant factors, Paulis I/X/Z): the complex64
+                                   chi >= 16 energy sweeps then accumulate real parts only (their
+                                   imaginary parts are exact zeros; results bit-identical) */
+  int32_t reserved;
 } tq_chain;
 
 /* Bytes of device workspace one call needs. */

@@ -42,6 +42,7 @@ class TqChain(ctypes.Structure):
         ("blob", ctypes.c_void_p), ("blob_off", ctypes.c_void_p),
         ("blob_max", ctypes.c_int32), ("blob_dtype", ctypes.c_int32),
         ("max_pairs", ctypes.c_int32), ("max_ttree", ctypes.c_int32),
+        ("real_path", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -290,6 +291,7 @@ class DevicePlan:
         ch.blob_dtype = code
         ch.max_pairs = int((plan.sites["chi_l"] * plan.sites["chi_r"]).max()) if len(plan.sites) else 1
         ch.max_ttree = int(plan.max_ttree)
+        ch.real_path = int(C.real_path(plan))
         self.chain = ch
         self._ws = {}
 

@@ -554,6 +554,26 @@ def _max_edges(sites):
     return m
 
 
+def real_path(plan) -> bool:
+    """True when every factor matrix, input vector and MPO edge of the plan is real (ry
+    rotations, real constant factors such as the CZ / CNOT projector splits, Paulis I/X/Z with
+    real coefficients): the energy sweeps' complex arithmetic then has exactly-zero imaginary
+    parts, and the engine runs its real-part instantiation (tq_chain.real_path)."""
+    mats = plan.mats
+    if len(mats):
+        kind = mats["kind"]
+        if not np.all((kind == 0) | (kind == 2)):
+            return False
+        const = mats["m"][kind == 0]
+        if const.size and np.any(const.reshape(len(const), -1)[:, 1::2] != 0):
+            return False
+    if len(plan.sites) and np.any(plan.sites["init"][:, [1, 3]] != 0):
+        return False
+    if len(plan.edges) and np.any(plan.edges["op"] == 2):
+        return False
+    return True
+
+
 def _edge(a, b, op, coef):
     e = np.zeros((), dtype=EDGE_DTYPE)
     e["a"], e["b"], e["op"], e["coef"] = a, b, op, coef

@@ -823,8 +823,19 @@ __device__ __forceinline__ void pair_adjoint_warp(int nops, int al, int be, cons
 //   C_t[m x n] = sum_{q < nq} A_{t,q}[m x kk] * B_{t,q}[kk x n]   (all row stride LD)
 // Each item computes rt consecutive rows of one column; a warp's lanes walk columns so the
 // A operand is a broadcast and the B operand a contiguous row.
-template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, bool HERM = false, typename FA,
-          typename FB, typename FS>
+// Complex multiply-accumulate of the GEMMs (K: 0 a*b, 1 conj(a)*b, 2 a*conj(b)), or with RE the
+// real part alone: the real-path sweeps (tq_chain.real_path) hold complex operands whose
+// imaginary parts are exact zeros, so the real FMA chain is the complex one's real part, bit for bit.
+template <bool RE, int K, typename C>
+__device__ __forceinline__ void gmac(C& acc, C a, C b) {
+  if constexpr (RE) acc.x = fma(a.x, b.x, acc.x);
+  else if constexpr (K == 0) cfma(acc, a, b);
+  else if constexpr (K == 1) cfmac(acc, a, b);
+  else cfmacb(acc, a, b);
+}
+
+template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, bool HERM = false, bool RE = false,
+          typename FA, typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
   // CTA: the A operand is stored as X (kk x m) and used as X^H; CTB likewise for B (n x kk).
   // HERM: every output C_t is Hermitian (m == n): only the tiles touching the upper triangle are
@@ -857,11 +868,11 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
             if (CTB) { b0 = cconj(b0); b1 = cconj(b1); }
             const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
             if (CTA) {
-              cfmac(c00, a0, b0); cfmac(c10, a1, b0); cfmac(c20, a2, b0); cfmac(c30, a3, b0);
-              cfmac(c01, a0, b1); cfmac(c11, a1, b1); cfmac(c21, a2, b1); cfmac(c31, a3, b1);
+              gmac<RE, 1>(c00, a0, b0); gmac<RE, 1>(c10, a1, b0); gmac<RE, 1>(c20, a2, b0); gmac<RE, 1>(c30, a3, b0);
+              gmac<RE, 1>(c01, a0, b1); gmac<RE, 1>(c11, a1, b1); gmac<RE, 1>(c21, a2, b1); gmac<RE, 1>(c31, a3, b1);
             } else {
-              cfma(c00, a0, b0); cfma(c10, a1, b0); cfma(c20, a2, b0); cfma(c30, a3, b0);
-              cfma(c01, a0, b1); cfma(c11, a1, b1); cfma(c21, a2, b1); cfma(c31, a3, b1);
+              gmac<RE, 0>(c00, a0, b0); gmac<RE, 0>(c10, a1, b0); gmac<RE, 0>(c20, a2, b0); gmac<RE, 0>(c30, a3, b0);
+              gmac<RE, 0>(c01, a0, b1); gmac<RE, 0>(c11, a1, b1); gmac<RE, 0>(c21, a2, b1); gmac<RE, 0>(c31, a3, b1);
             }
           }
         }
@@ -904,11 +915,11 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
           if (CTB) { b0 = cconj(b0); b1 = cconj(b1); }
           const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
           if (CTA) {
-            cfmac(c00, a0, b0); cfmac(c10, a1, b0); cfmac(c20, a2, b0); cfmac(c30, a3, b0);
-            cfmac(c01, a0, b1); cfmac(c11, a1, b1); cfmac(c21, a2, b1); cfmac(c31, a3, b1);
+            gmac<RE, 1>(c00, a0, b0); gmac<RE, 1>(c10, a1, b0); gmac<RE, 1>(c20, a2, b0); gmac<RE, 1>(c30, a3, b0);
+            gmac<RE, 1>(c01, a0, b1); gmac<RE, 1>(c11, a1, b1); gmac<RE, 1>(c21, a2, b1); gmac<RE, 1>(c31, a3, b1);
           } else {
-            cfma(c00, a0, b0); cfma(c10, a1, b0); cfma(c20, a2, b0); cfma(c30, a3, b0);
-            cfma(c01, a0, b1); cfma(c11, a1, b1); cfma(c21, a2, b1); cfma(c31, a3, b1);
+            gmac<RE, 0>(c00, a0, b0); gmac<RE, 0>(c10, a1, b0); gmac<RE, 0>(c20, a2, b0); gmac<RE, 0>(c30, a3, b0);
+            gmac<RE, 0>(c01, a0, b1); gmac<RE, 0>(c11, a1, b1); gmac<RE, 0>(c21, a2, b1); gmac<RE, 0>(c31, a3, b1);
           }
         }
       }
@@ -953,12 +964,12 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
           const C bv = Bb[k * sb];
           const C a0 = Ab[k * sa], a1 = Ab[ra + k * sa], a2 = Ab[2 * ra + k * sa], a3 = Ab[3 * ra + k * sa];
           if (CTA) {
-            if (CTB) { C cb = cconj(bv); cfmac(acc0, a0, cb); cfmac(acc1, a1, cb); cfmac(acc2, a2, cb); cfmac(acc3, a3, cb); }
-            else { cfmac(acc0, a0, bv); cfmac(acc1, a1, bv); cfmac(acc2, a2, bv); cfmac(acc3, a3, bv); }
+            if (CTB) { C cb = cconj(bv); gmac<RE, 1>(acc0, a0, cb); gmac<RE, 1>(acc1, a1, cb); gmac<RE, 1>(acc2, a2, cb); gmac<RE, 1>(acc3, a3, cb); }
+            else { gmac<RE, 1>(acc0, a0, bv); gmac<RE, 1>(acc1, a1, bv); gmac<RE, 1>(acc2, a2, bv); gmac<RE, 1>(acc3, a3, bv); }
           } else if (CTB) {
-            cfmacb(acc0, a0, bv); cfmacb(acc1, a1, bv); cfmacb(acc2, a2, bv); cfmacb(acc3, a3, bv);
+            gmac<RE, 2>(acc0, a0, bv); gmac<RE, 2>(acc1, a1, bv); gmac<RE, 2>(acc2, a2, bv); gmac<RE, 2>(acc3, a3, bv);
           } else {
-            cfma(acc0, a0, bv); cfma(acc1, a1, bv); cfma(acc2, a2, bv); cfma(acc3, a3, bv);
+            gmac<RE, 0>(acc0, a0, bv); gmac<RE, 0>(acc1, a1, bv); gmac<RE, 0>(acc2, a2, bv); gmac<RE, 0>(acc3, a3, bv);
           }
         }
       } else {
@@ -966,10 +977,10 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
           const C bv = Bb[k * sb];
           const C a0 = Ab[k * sa];
           const C b2 = CTB ? cconj(bv) : bv;
-          if (CTA) cfmac(acc0, a0, b2); else cfma(acc0, a0, b2);
+          if (CTA) gmac<RE, 1>(acc0, a0, b2); else gmac<RE, 0>(acc0, a0, b2);
           if (rt == 2) {
             const C a1 = Ab[ra + k * sa];
-            if (CTA) cfmac(acc1, a1, b2); else cfma(acc1, a1, b2);
+            if (CTA) gmac<RE, 1>(acc1, a1, b2); else gmac<RE, 0>(acc1, a1, b2);
           }
         }
       }
@@ -1251,7 +1262,7 @@ __device__ __forceinline__ const C* wct_row_of(const Params& p, int site, int di
 #ifndef TQ_LR_MINB
 #define TQ_LR_MINB 4
 #endif
-template <typename R, int CHI, int TEAM, int FD>
+template <typename R, int CHI, int TEAM, int FD, bool RE = false>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_RL_MINB : 4) : 1)
 rl_sweep(Params p) {
   using C = typename CT<R>::T;
@@ -1343,7 +1354,7 @@ rl_sweep(Params p) {
       STAGE(2);
     } else {
       // N[b][s] = A[s] * P[b]
-      gemm_group<C, LD, TEAM>(tid, db * 2, cl, cr, cr, 1,
+      gemm_group<C, LD, TEAM, false, false, false, RE>(tid, db * 2, cl, cr, cr, 1,
             [&](int t, int) { return Acur + (t & 1) * MS; },
             [&](int t, int) { return PIN + (t >> 1) * MS; },
             [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
@@ -1397,7 +1408,7 @@ rl_sweep(Params p) {
           }
         }
       } else {
-        gemm_group<C, LD, TEAM / 2, false, true, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+        gemm_group<C, LD, TEAM / 2, false, true, true, RE>(tid, da, cl, cl, cr, 2, pa, pb, ps);
       }
       team_sync<TEAM>();
       STAGE(4);
@@ -1417,8 +1428,8 @@ rl_sweep(Params p) {
     // P'[a] = sum_s' BR[a][s'] AH[s']  -> PIN slots (P[b] is dead) + HBM
     {
       // the environments of the energy / gradient MPO are Hermitian (real coefficients): half the work
-      if (CHI >= 16 && p.mode == 0) gemm_group<C, LD, TEAM, false, true, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
-      else gemm_group<C, LD, TEAM, false, true>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+      if (CHI >= 16 && p.mode == 0) gemm_group<C, LD, TEAM, false, true, true, RE>(tid, da, cl, cl, cr, 2, pa, pb, ps);
+      else gemm_group<C, LD, TEAM, false, true, false, RE>(tid, da, cl, cl, cr, 2, pa, pb, ps);
     }
     STAGE(5);
     // warp teams: resolve the next site's descriptors after the GEMM (independent work)
@@ -1440,7 +1451,7 @@ rl_sweep(Params p) {
 // ------------------------------------------------------------------ left-to-right sweep
 // MODE 0: gradient (G + column adjoint); MODE 1: per-term values.  Separate instantiations
 // keep each kernel's code small enough for the instruction cache.
-template <typename R, int CHI, int TEAM, int MODE, int FD>
+template <typename R, int CHI, int TEAM, int MODE, int FD, bool RE = false>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_LR_MINB : 4) : 1)
 lr_sweep(Params p) {
   using C = typename CT<R>::T;
@@ -1575,7 +1586,7 @@ lr_sweep(Params p) {
       STAGE(2);
     } else {
       // M[a][s] = Lam[a] * A[s]
-      gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cl, 1,
+      gemm_group<C, LD, TEAM, false, false, false, RE>(tid, da * 2, cl, cr, cl, 1,
           [&](int t, int) { return LAM + (t >> 1) * MS; },
           [&](int t, int) { return Acur + (t & 1) * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
@@ -1613,11 +1624,11 @@ lr_sweep(Params p) {
       auto ls = [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(LAM + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); };
       if constexpr (SPLIT) {
         if (tid < TEAM / 2) {
-          gemm_group<C, LD, TEAM / 2, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
+          gemm_group<C, LD, TEAM / 2, true, false, true, RE>(tid, db, cr, cr, cl, 2, la, lb, ls);
         } else {   // G[s'] = sum_bb BR[bb][s'] PIN[bb], straight from the epilogue to HBM (dense [2][cl][cr])
           C* const gg = env_g_w + st.g_off;
           const int np = cl * cr;
-          gemm_group<C, LD, TEAM / 2>(tid - TEAM / 2, 2, cl, cr, cr, db,
+          gemm_group<C, LD, TEAM / 2, false, false, false, RE>(tid - TEAM / 2, 2, cl, cr, cr, db,
               [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
               [&](int, int qq) { return PIN + qq * MS; },
               [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) {
@@ -1626,9 +1637,9 @@ lr_sweep(Params p) {
               });
         }
       } else if (CHI >= 16 && MODE == 0) {
-        gemm_group<C, LD, TEAM, true, false, true>(tid, db, cr, cr, cl, 2, la, lb, ls);
+        gemm_group<C, LD, TEAM, true, false, true, RE>(tid, db, cr, cr, cl, 2, la, lb, ls);
       } else {
-        gemm_group<C, LD, TEAM, true, false>(tid, db, cr, cr, cl, 2, la, lb, ls);
+        gemm_group<C, LD, TEAM, true, false, false, RE>(tid, db, cr, cr, cl, 2, la, lb, ls);
       }
     }
     if (TEAM < 128 && has_next) {   // warp teams: next site's descriptors, overlapped with this site's GEMMs
@@ -1645,7 +1656,7 @@ lr_sweep(Params p) {
         team_sync<TEAM>();
       }
       // G[s'] = sum_bb BR[bb][s'] PIN[bb]   (writes over M, read only by the bracket stage)
-      if (!SPLIT && !(FUSE && p.L.direct)) gemm_group<C, LD, TEAM>(tid, 2, cl, cr, cr, db,
+      if (!SPLIT && !(FUSE && p.L.direct)) gemm_group<C, LD, TEAM, false, false, false, RE>(tid, 2, cl, cr, cr, db,
           [&](int t, int qq) { return sm.BR + (qq * 2 + t) * MS; },
           [&](int, int qq) { return PIN + qq * MS; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(G + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
@@ -1681,7 +1692,7 @@ lr_sweep(Params p) {
       STAGE(5);
     } else {
       // ---- values: rho_a[s'][s] = <A[s'], M[a][s] R> for every source channel a
-      gemm_group<C, LD, TEAM>(tid, da * 2, cl, cr, cr, 1,
+      gemm_group<C, LD, TEAM, false, false, false, RE>(tid, da * 2, cl, cr, cr, 1,
           [&](int t, int) { return M + t * MS; },
           [&](int, int) { return PIN; },
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(sm.MR + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
@@ -2222,9 +2233,14 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     q.L = make_layout(&prm.c, CHI, TEAM, sizeof(R), false, prm.mode);
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
-    set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED>), smem);
     if (g_timing.on) cudaEventRecord(g_timing.ev[0], s);
-    rl_sweep<R, CHI, TEAM, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    if (CHI >= 16 && sizeof(R) == 4 && prm.c.real_path && prm.mode == 0) {
+      set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED, CHI >= 16 && sizeof(R) == 4>), smem);
+      rl_sweep<R, CHI, TEAM, FUSED, CHI >= 16 && sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    } else {
+      set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED>), smem);
+      rl_sweep<R, CHI, TEAM, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    }
     if (g_timing.on) cudaEventRecord(g_timing.ev[1], s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
@@ -2235,7 +2251,10 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
     if (g_timing.on) cudaEventRecord(g_timing.ev[2], s);
-    if (prm.mode == 0) {
+    if (prm.mode == 0 && CHI >= 16 && sizeof(R) == 4 && prm.c.real_path) {
+      set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED, CHI >= 16 && sizeof(R) == 4>), smem);
+      lr_sweep<R, CHI, TEAM, 0, FUSED, CHI >= 16 && sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    } else if (prm.mode == 0) {
       set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED>), smem);
       lr_sweep<R, CHI, TEAM, 0, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
     } else {
