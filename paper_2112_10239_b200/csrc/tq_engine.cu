@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void bracket_stage(int tid, int ntarget, int ec, cons
 // launch by build_wct, or per site by stage_blob): every thread owns two (i, j) elements and
 // forms all (target, s') outputs from all (source, s) inputs in registers, skipping channel pairs
 // the mask marks empty.  chi >= 16 (the per-edge loop of bracket_stage is latency bound there).
-template <typename R, int LD, int TEAM, int DM>
+template <typename R, int LD, int TEAM, int DM, bool RE = false>
 __device__ __forceinline__ void wbracket_stage(int tid, int nsrc, int ntgt, const typename CT<R>::T* SRC,
                                                const typename CT<R>::T* wc, typename CT<R>::T* BR, int lcl, int lcr) {
   using C = typename CT<R>::T;
@@ -1111,8 +1111,8 @@ __device__ __forceinline__ void wbracket_stage(int tid, int nsrc, int ntgt, cons
         const C w00 = w[0], w01 = w[1], w10 = w[2], w11 = w[3];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          cfma(o[u][0], w00, v[u][xs][0]); cfma(o[u][0], w01, v[u][xs][1]);
-          cfma(o[u][1], w10, v[u][xs][0]); cfma(o[u][1], w11, v[u][xs][1]);
+          gmac<RE, 0>(o[u][0], w00, v[u][xs][0]); gmac<RE, 0>(o[u][0], w01, v[u][xs][1]);
+          gmac<RE, 0>(o[u][1], w10, v[u][xs][0]); gmac<RE, 0>(o[u][1], w11, v[u][xs][1]);
         }
       }
 #pragma unroll
@@ -1360,7 +1360,7 @@ rl_sweep(Params p) {
             [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(N + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
-      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM>(tid, db, da, N, WC, sm.BR, lcl, lcr);
+      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM, RE>(tid, db, da, N, WC, sm.BR, lcl, lcr);
       else bracket_stage<R, LD, TEAM>(tid, da, st.rl_edge_count, sm.sedge, true, N, sm.BR, lcl, lcr);
       blob_wait();
       team_sync<TEAM>();
@@ -1592,7 +1592,7 @@ lr_sweep(Params p) {
           [&](int t, int i0, int j, int rt, C a0, C a1, C a2, C a3) { store_rows<C, LD>(M + t * MS + i0 * LD + j, rt, a0, a1, a2, a3); });
       team_sync<TEAM>();
       STAGE(2);
-      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM>(tid, da, db, M, WC, sm.BR, lcl, lcr);
+      if constexpr (WBR) wbracket_stage<R, LD, TEAM, FDM, RE>(tid, da, db, M, WC, sm.BR, lcl, lcr);
       else bracket_stage<R, LD, TEAM>(tid, db, st.lr_edge_count, sm.sedge, false, M, sm.BR, lcl, lcr);
       if (!pf2) blob_wait();   // pf2: the blob landed with A(q) at the site's start
       team_sync<TEAM>();

@@ -184,3 +184,19 @@ def test_taped_truncation_rule():
     assert AD._taped_truncates(bw, 1e-3, None)       # eps > 0 may cut anywhere
     c = layered_circuit(6, 2)                        # one entangler line: taped bonds stay 2
     assert not AD._taped_truncates(c, 0.0, 2)
+
+
+def test_real_path_flag():
+    """chain.real_path (tq_chain.real_path): real iff every factor, input vector and MPO edge is
+    real -- ry + CZ/CNOT + X/Z terms yes; rx / rz rotations or a Y term no."""
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200.hamiltonians import PauliHamiltonian, term, tfim
+    from paper_2112_10239_b200.workloads import layered_circuit
+
+    def flag(rot, ent, ham):
+        return C.real_path(C.compile_chain(layered_circuit(10, 4, rot, ent), C.normalize_terms(ham), "energy"))
+
+    assert flag("ry", "cz", tfim(10)) and flag("ry", "cnot", tfim(10))
+    assert not flag("rx", "cz", tfim(10)) and not flag("rz", "cnot", tfim(10))
+    ham_y = PauliHamiltonian(10, tfim(10).terms + (term(0.5, ((3, "Y"), (4, "Y"))),))
+    assert not flag("ry", "cz", ham_y)
