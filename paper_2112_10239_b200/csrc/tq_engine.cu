@@ -63,6 +63,17 @@ template <typename C> __device__ __forceinline__ void cfmacb(C& acc, C a, C b) {
 }
 
 // ------------------------------------------------------------------ kernel parameters
+// Complex multiply-accumulate of the GEMMs (K: 0 a*b, 1 conj(a)*b, 2 a*conj(b)), or with RE the
+// real part alone: the real-path sweeps (tq_chain.real_path) hold complex operands whose
+// imaginary parts are exact zeros, so the real FMA chain is the complex one's real part, bit for bit.
+template <bool RE, int K, typename C>
+__device__ __forceinline__ void gmac(C& acc, C a, C b) {
+  if constexpr (RE) acc.x = fma(a.x, b.x, acc.x);
+  else if constexpr (K == 0) cfma(acc, a, b);
+  else if constexpr (K == 1) cfmac(acc, a, b);
+  else cfmacb(acc, a, b);
+}
+
 struct Layout {          // byte offsets inside one team's shared-memory slab (host computed)
   int32_t a, ah, env, m, br, pin, mr, contrib, mres, minfo, mps, ocode, ogidx, obase, sedge;
   int32_t tree;          // 0: per-pair column walks; 1: digit tree, dedicated levels; 2: digit tree in M/BR scratch
@@ -617,7 +628,7 @@ __device__ void fold_site4r(const tq_chain& ch, const tq_site& st, int tid, cons
 // ping-pong through two scratch buffers of 2^(bits) vectors, which the backward walk then reuses
 // for U.  cfg4: 16 KB of kept levels instead of 49 KB for all of them, so four 128-thread units
 // fit on an SM.
-template <typename R, int TEAM>
+template <typename R, int TEAM, bool RE = false>
 __device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::T* mres, const int* ocode,
                               typename CT<R>::T* levt, typename CT<R>::T* scratch, int* tbase) {
   using C = typename CT<R>::T;
@@ -641,8 +652,14 @@ __device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::
       const C v1 = src ? src[2 * idx + 1] : i1;
       for (int d = 0; d < nd; ++d) {
         const C* M = Mb + 4 * d;
-        C n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
-        C n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
+        C n0, n1;
+        if constexpr (RE) {   // real path: the complex product's real part, bit for bit
+          n0 = cmk<C>(fma(M[1].x, v1.x, M[0].x * v0.x), R(0));
+          n1 = cmk<C>(fma(M[3].x, v1.x, M[2].x * v0.x), R(0));
+        } else {
+          n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
+          n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
+        }
         const int e = idx + (d << toff);
         dst[2 * e] = n0; dst[2 * e + 1] = n1;
       }
@@ -665,7 +682,7 @@ __device__ __forceinline__ int tree_index(const int* ocode, int nops, int al, in
 // of the core cotangent (G[0], G[1])[alpha][beta] (read straight from HBM, dense [2][cl][cr]);
 // walking down, every trainable rotation accumulates Im<U_l, sigma V_l> (per-warp partials in
 // contrib) and U_{l-1}[idx] = sum_d M_l(d)^H U_l[idx | d << toff_l].
-template <typename R, int TEAM>
+template <typename R, int TEAM, bool RE = false>
 __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
                               const int* minfo, const int* ocode, const typename CT<R>::T* levt, const int* tbase,
                               typename CT<R>::T* ua, int* tal, const typename CT<R>::T* gg, int lcr, R* contrib) {
@@ -730,6 +747,10 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
         if (kind == 0) continue;
         const C u0 = ua[2 * e], u1 = ua[2 * e + 1];
         const C v0 = V[2 * e], v1 = V[2 * e + 1];
+        if constexpr (RE) {   // real path: only ry (sigma = Y) is trainable; Im<u, Y v> in real terms
+          acc += fma(u1.x, v0.x, -u0.x * v1.x);
+          continue;
+        }
         C s0, s1;
         if (kind == 1) { s0 = v1; s1 = v0; }
         else if (kind == 2) { s0 = cmk<C>(v1.y, -v1.x); s1 = cmk<C>(-v0.y, v0.x); }
@@ -750,8 +771,8 @@ __device__ void ctree_adjoint(const tq_chain& ch, const tq_site& st, int tid, co
         for (int d = 0; d < (1 << bits); ++d) {
           const C* M = mres + 4 * (lm + d);
           const C u0 = ua[2 * (idx | (d << toff))], u1 = ua[2 * (idx | (d << toff)) + 1];
-          cfmac(w0, M[0], u0); cfmac(w0, M[2], u1);
-          cfmac(w1, M[1], u0); cfmac(w1, M[3], u1);
+          gmac<RE, 1>(w0, M[0], u0); gmac<RE, 1>(w0, M[2], u1);
+          gmac<RE, 1>(w1, M[1], u0); gmac<RE, 1>(w1, M[3], u1);
         }
         ua[2 * idx] = w0; ua[2 * idx + 1] = w1;
       }
@@ -823,17 +844,6 @@ __device__ __forceinline__ void pair_adjoint_warp(int nops, int al, int be, cons
 //   C_t[m x n] = sum_{q < nq} A_{t,q}[m x kk] * B_{t,q}[kk x n]   (all row stride LD)
 // Each item computes rt consecutive rows of one column; a warp's lanes walk columns so the
 // A operand is a broadcast and the B operand a contiguous row.
-// Complex multiply-accumulate of the GEMMs (K: 0 a*b, 1 conj(a)*b, 2 a*conj(b)), or with RE the
-// real part alone: the real-path sweeps (tq_chain.real_path) hold complex operands whose
-// imaginary parts are exact zeros, so the real FMA chain is the complex one's real part, bit for bit.
-template <bool RE, int K, typename C>
-__device__ __forceinline__ void gmac(C& acc, C a, C b) {
-  if constexpr (RE) acc.x = fma(a.x, b.x, acc.x);
-  else if constexpr (K == 0) cfma(acc, a, b);
-  else if constexpr (K == 1) cfmac(acc, a, b);
-  else cfmacb(acc, a, b);
-}
-
 template <typename C, int LD, int TEAM, bool CTA = false, bool CTB = false, bool HERM = false, bool RE = false,
           typename FA, typename FB, typename FS>
 __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, int kk, int nq, FA fa, FB fb, FS store) {
@@ -1779,7 +1789,7 @@ struct AdjLayout {
 #ifndef TQ_ADJ128_MINB
 #define TQ_ADJ128_MINB 4
 #endif
-template <typename R, int CHI, int TEAM>
+template <typename R, int CHI, int TEAM, bool RE = false>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM, TEAM == 32 ? (sizeof(R) == 4 ? TQ_ADJ_MINB : 4) : (TEAM == 128 ? (sizeof(R) == 4 ? TQ_ADJ128_MINB : 4) : 1))
 adj_sweep(Params p, AdjLayout A) {
   using C = typename CT<R>::T;
@@ -1862,8 +1872,8 @@ adj_sweep(Params p, AdjLayout A) {
       C* u0 = reinterpret_cast<C*>(base + A.ubuf);       // forward scratch, then U (in place)
       int* tal = reinterpret_cast<int*>(base + A.utab);
       int* tbase = obase;   // host tbase offsets are for the full tree; the compact ones go here
-      ctree_forward<R, TEAM>(st, tid, mres, ocode, lev, u0, tbase);
-      ctree_adjoint<R, TEAM>(p.c, st, tid, mres, minfo, ocode, lev, tbase, u0, tal, gg, lcr, contrib);
+      ctree_forward<R, TEAM, RE>(st, tid, mres, ocode, lev, u0, tbase);
+      ctree_adjoint<R, TEAM, RE>(p.c, st, tid, mres, minfo, ocode, lev, tbase, u0, tal, gg, lcr, contrib);
     }
   }
   const bool one_pair = np <= TEAM;
@@ -2271,9 +2281,15 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
       const size_t asmem = (size_t)A.team_bytes * ATEAMS;
       if (asmem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "adjoint shared-memory layout exceeds 227 KB");
       const int64_t units = (int64_t)prm.batch * prm.c.n_sites;
-      set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM>), asmem);
+      const unsigned agrid = (unsigned)((units + ATEAMS - 1) / ATEAMS);
       if (g_timing.on) cudaEventRecord(g_timing.ev[4], s);
-      adj_sweep<R, CHI, ATEAM><<<(unsigned)((units + ATEAMS - 1) / ATEAMS), ATEAM * ATEAMS, asmem, s>>>(prm, A);
+      if (CHI >= 16 && sizeof(R) == 4 && prm.c.real_path && A.tree) {
+        set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM, CHI >= 16 && sizeof(R) == 4>), asmem);
+        adj_sweep<R, CHI, ATEAM, CHI >= 16 && sizeof(R) == 4><<<agrid, ATEAM * ATEAMS, asmem, s>>>(prm, A);
+      } else {
+        set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM>), asmem);
+        adj_sweep<R, CHI, ATEAM><<<agrid, ATEAM * ATEAMS, asmem, s>>>(prm, A);
+      }
       if (g_timing.on) cudaEventRecord(g_timing.ev[5], s);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail(TQ_ERR_CUDA, cudaGetErrorString(e));
