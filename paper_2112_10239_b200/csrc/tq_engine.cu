@@ -2244,9 +2244,9 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
     if (g_timing.on) cudaEventRecord(g_timing.ev[0], s);
-    if (CHI >= 16 && sizeof(R) == 4 && prm.c.real_path && prm.mode == 0) {
-      set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED, CHI >= 16 && sizeof(R) == 4>), smem);
-      rl_sweep<R, CHI, TEAM, FUSED, CHI >= 16 && sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    if (sizeof(R) == 4 && prm.c.real_path && prm.mode == 0) {
+      set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED, sizeof(R) == 4>), smem);
+      rl_sweep<R, CHI, TEAM, FUSED, sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
     } else {
       set_smem_attr(reinterpret_cast<const void*>(rl_sweep<R, CHI, TEAM, FUSED>), smem);
       rl_sweep<R, CHI, TEAM, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
@@ -2261,9 +2261,9 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
     const size_t smem = (size_t)q.L.team_bytes * TEAMS;
     if (smem > 227 * 1024) return fail(TQ_ERR_UNSUPPORTED, "shared-memory layout exceeds 227 KB (too many MPO channels for this bond dimension)");
     if (g_timing.on) cudaEventRecord(g_timing.ev[2], s);
-    if (prm.mode == 0 && CHI >= 16 && sizeof(R) == 4 && prm.c.real_path) {
-      set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED, CHI >= 16 && sizeof(R) == 4>), smem);
-      lr_sweep<R, CHI, TEAM, 0, FUSED, CHI >= 16 && sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
+    if (prm.mode == 0 && sizeof(R) == 4 && prm.c.real_path) {
+      set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED, sizeof(R) == 4>), smem);
+      lr_sweep<R, CHI, TEAM, 0, FUSED, sizeof(R) == 4><<<grid, TEAM * TEAMS, smem, s>>>(q);
     } else if (prm.mode == 0) {
       set_smem_attr(reinterpret_cast<const void*>(lr_sweep<R, CHI, TEAM, 0, FUSED>), smem);
       lr_sweep<R, CHI, TEAM, 0, FUSED><<<grid, TEAM * TEAMS, smem, s>>>(q);
@@ -2283,9 +2283,9 @@ static tq_status launch_pair_f(Params& prm, bool run_lr, cudaStream_t s) {
       const int64_t units = (int64_t)prm.batch * prm.c.n_sites;
       const unsigned agrid = (unsigned)((units + ATEAMS - 1) / ATEAMS);
       if (g_timing.on) cudaEventRecord(g_timing.ev[4], s);
-      if (CHI >= 16 && sizeof(R) == 4 && prm.c.real_path && A.tree) {
-        set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM, CHI >= 16 && sizeof(R) == 4>), asmem);
-        adj_sweep<R, CHI, ATEAM, CHI >= 16 && sizeof(R) == 4><<<agrid, ATEAM * ATEAMS, asmem, s>>>(prm, A);
+      if (sizeof(R) == 4 && prm.c.real_path && A.tree) {
+        set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM, sizeof(R) == 4>), asmem);
+        adj_sweep<R, CHI, ATEAM, sizeof(R) == 4><<<agrid, ATEAM * ATEAMS, asmem, s>>>(prm, A);
       } else {
         set_smem_attr(reinterpret_cast<const void*>(adj_sweep<R, CHI, ATEAM>), asmem);
         adj_sweep<R, CHI, ATEAM><<<agrid, ATEAM * ATEAMS, asmem, s>>>(prm, A);
