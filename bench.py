@@ -274,7 +274,10 @@ def work_model(cfg, circuit, ham, batch):
     t1 = sum(1 for _, ops in terms if len(ops) == 1)
     t2 = sum(1 for _, ops in terms if len(ops) == 2)
     plan1 = C.compile_chain(circuit, terms, "energy", batch=batch, segments=1)
-    return roofline.survey_model(plan1, t1, t2, cfg.layers, cfg.grad), roofline.eval_model(plan1, grad=cfg.grad)
+    # the bench arm computes in complex64: real-path plans run the real-part instantiation
+    real = bool(C.real_path(plan1)) and plan1.mode != "values"
+    return (roofline.survey_model(plan1, t1, t2, cfg.layers, cfg.grad),
+            roofline.eval_model(plan1, grad=cfg.grad, real=real))
 
 
 def run_ours(args, cfg):
@@ -520,12 +523,15 @@ def run_ours(args, cfg):
                      "executed_model": {"flops_rl": executed["flops_rl"], "flops_lr": executed["flops_lr"],
                                         "flops_adj": executed["flops_adj"],
                                         "flops_per_launch": exec_flops, "achieved": exec_tf,
+                                        "real_path": executed["real_path"],
+                                        "flops_per_cmac": executed["flops_per_cmac"],
                                         "frac": exec_tf / peak_fp32 if peak_fp32 else None,
                                         "note": "roofline.eval_model: cMACs the kernels issue (unsegmented chain, "
                                                 "Hermitian transfers on upper tiles). 8(d)'s F counts every "
                                                 "transfer in full, so its frac can exceed 1 where the kernels "
                                                 "skip work the formula counts; this frac is the FFMA share the "
-                                                "useful executed work reaches"}},
+                                                "useful executed work reaches (real_path: 2 flops per cMAC, the "
+                                                "one real FMA the real-part instantiation issues)"}},
         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
                 "bytes_per_step": step_bytes, "B_eval": survey["B_eval"],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs", "work_model": "SURVEY.md 8(d) B_eval"},

@@ -70,18 +70,24 @@ def env_bytes(plan, real_bytes: int = 4) -> float:
     return float(plan.env_total) * 2 * real_bytes
 
 
-def eval_model(plan, grad: bool = True, real_bytes: int = 4) -> dict:
-    """Per-evaluation (one theta-set) flops and compulsory HBM bytes."""
+def eval_model(plan, grad: bool = True, real_bytes: int = 4, real: bool = False) -> dict:
+    """Per-evaluation (one theta-set) flops and compulsory HBM bytes.
+
+    ``real``: the plan runs the engine's real-path instantiation (tq_chain.real_path,
+    complex64 energy mode; chain.real_path): every operand's imaginary part is an exact
+    zero and the kernels issue one real FMA (2 flops) per cMAC instead of 8 flops."""
     c = sweep_cmacs(plan)
-    flops_rl = 8 * c["rl"]
-    flops_lr = 8 * c["lr"] if grad else 0.0
-    flops_adj = 8 * c["adj"] if grad else 0.0
+    per = 2.0 if real else 8.0
+    flops_rl = per * c["rl"]
+    flops_lr = per * c["lr"] if grad else 0.0
+    flops_adj = per * c["adj"] if grad else 0.0
     P = plan.n_params
     byts = P * real_bytes + 16
     if grad:
         byts += P * real_bytes + 2 * env_bytes(plan, real_bytes)
     return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops_adj": flops_adj,
-            "flops": flops_rl + flops_lr + flops_adj, "bytes": byts, "cmacs": c}
+            "flops": flops_rl + flops_lr + flops_adj, "bytes": byts, "cmacs": c,
+            "flops_per_cmac": per, "real_path": bool(real)}
 
 
 def survey_model(plan, n_terms_1: int, n_terms_2: int, layers: int, grad: bool = True) -> dict:

@@ -200,3 +200,19 @@ def test_real_path_flag():
     assert not flag("rx", "cz", tfim(10)) and not flag("rz", "cnot", tfim(10))
     ham_y = PauliHamiltonian(10, tfim(10).terms + (term(0.5, ((3, "Y"), (4, "Y"))),))
     assert not flag("ry", "cz", ham_y)
+
+
+def test_executed_model_counts_real_fmas_on_real_path():
+    """bench.py's executed-work model charges 2 flops per cMAC (one real FMA) when the plan runs
+    the real-part instantiation, 8 otherwise; the cMAC count itself is unchanged."""
+    import bench
+    from paper_2112_10239_b200 import chain as C
+    from paper_2112_10239_b200 import roofline
+    from paper_2112_10239_b200.workloads import CONFIGS
+
+    cfg = CONFIGS["cfg2"]
+    _, e = bench.work_model(cfg, cfg.circuit(), cfg.hamiltonian(), cfg.batch)
+    plan = C.compile_chain(cfg.circuit(), C.normalize_terms(cfg.hamiltonian()), "energy", segments=1)
+    full = roofline.eval_model(plan, grad=True)
+    assert e["real_path"] and e["flops_per_cmac"] == 2.0 and not full["real_path"]
+    assert abs(e["flops"] * 4 - full["flops"]) < 1e-6 * full["flops"]
