@@ -75,19 +75,22 @@ def eval_model(plan, grad: bool = True, real_bytes: int = 4, real: bool = False)
 
     ``real``: the plan runs the engine's real-path instantiation (tq_chain.real_path,
     complex64 energy mode; chain.real_path): every operand's imaginary part is an exact
-    zero and the kernels issue one real FMA (2 flops) per cMAC instead of 8 flops."""
+    zero and the sweeps issue one real FMA (2 flops) per cMAC instead of 8 flops; the column
+    adjoint's real instantiation exists for the digit-tree layout only (chi_max >= 16,
+    tq_engine.cu make_adj_layout), the chi <= 8 warp adjoint stays complex."""
     c = sweep_cmacs(plan)
     per = 2.0 if real else 8.0
+    per_adj = 2.0 if real and plan.chi_max >= 16 else 8.0
     flops_rl = per * c["rl"]
     flops_lr = per * c["lr"] if grad else 0.0
-    flops_adj = per * c["adj"] if grad else 0.0
+    flops_adj = per_adj * c["adj"] if grad else 0.0
     P = plan.n_params
     byts = P * real_bytes + 16
     if grad:
         byts += P * real_bytes + 2 * env_bytes(plan, real_bytes)
     return {"flops_rl": flops_rl, "flops_lr": flops_lr, "flops_adj": flops_adj,
             "flops": flops_rl + flops_lr + flops_adj, "bytes": byts, "cmacs": c,
-            "flops_per_cmac": per, "real_path": bool(real)}
+            "flops_per_cmac": per, "flops_per_cmac_adj": per_adj, "real_path": bool(real)}
 
 
 def survey_model(plan, n_terms_1: int, n_terms_2: int, layers: int, grad: bool = True) -> dict:

@@ -215,4 +215,9 @@ def test_executed_model_counts_real_fmas_on_real_path():
     plan = C.compile_chain(cfg.circuit(), C.normalize_terms(cfg.hamiltonian()), "energy", segments=1)
     full = roofline.eval_model(plan, grad=True)
     assert e["real_path"] and e["flops_per_cmac"] == 2.0 and not full["real_path"]
-    assert abs(e["flops"] * 4 - full["flops"]) < 1e-6 * full["flops"]
+    assert abs(e["flops_rl"] * 4 - full["flops_rl"]) < 1e-6 * full["flops_rl"]
+    assert abs(e["flops_lr"] * 4 - full["flops_lr"]) < 1e-6 * full["flops_lr"]
+    assert e["flops_adj"] == full["flops_adj"]          # chi 8: the warp adjoint stays complex
+    c4 = CONFIGS["cfg4"]
+    _, e4 = bench.work_model(c4, c4.circuit(), c4.hamiltonian(), c4.batch)
+    assert e4["flops_per_cmac_adj"] == 2.0                 # chi 32: digit-tree adjoint, real
