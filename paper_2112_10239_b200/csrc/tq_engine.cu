@@ -30,6 +30,12 @@
 
 #include "../../include/tq_engine.h"
 
+#ifndef TQ_RE_TILE44
+#define TQ_RE_TILE44 1   // real-path 4x4 register tiles (0: the complex path's 4x2 tiling)
+#endif
+#ifndef TQ_RE_HERM44
+#define TQ_RE_HERM44 1   // real-path 4x4 tiles for the Hermitian X^H-operand GEMM (LR Lambda)
+#endif
 #ifndef TQ_TEAM32
 #define TQ_TEAM32 512   // threads per chi = 32 team (one CTA); same-box A/B cfg4: 512 3387, 384 3278, 256 3335 evals/s
 #endif
@@ -460,6 +466,18 @@ __device__ void fold_site(const tq_chain& ch, const tq_site& st, int tid, const 
   }
 }
 
+// Real parts of a resolved 2x2 factor (4 complex entries, 16-byte aligned in shared memory).
+// complex64: two 16-byte loads instead of four 4-byte ones (the fold is shared-memory bound).
+template <typename R>
+__device__ __forceinline__ void real_factor(const typename CT<R>::T* M, R& m0, R& m1, R& m2, R& m3) {
+  if constexpr (sizeof(R) == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(M), b = *reinterpret_cast<const float4*>(M + 2);
+    m0 = a.x; m1 = a.z; m2 = b.x; m3 = b.z;
+  } else {
+    m0 = M[0].x; m1 = M[1].x; m2 = M[2].x; m3 = M[3].x;
+  }
+}
+
 // fold_site (no AH) for a real column, as fold_site4r: real 2-vectors, 4 FMA per op, bit-identical.
 template <typename R, int LD, int TEAM>
 __device__ void fold_site_real(const tq_chain& ch, const tq_site& st, int tid, const typename CT<R>::T* mres,
@@ -475,8 +493,10 @@ __device__ void fold_site_real(const tq_chain& ch, const tq_site& st, int tid, c
       for (int oi = 0; oi < st.op_count; ++oi) {
         const int c = ocode[oi];
         const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al, be));
-        const R n0 = fma(M[1].x, v1, M[0].x * v0);
-        const R n1 = fma(M[3].x, v1, M[2].x * v0);
+        R m0, m1, m2, m3;
+        real_factor<R>(M, m0, m1, m2, m3);
+        const R n0 = fma(m1, v1, m0 * v0);
+        const R n1 = fma(m3, v1, m2 * v0);
         v0 = n0; v1 = n1;
       }
     }
@@ -600,7 +620,8 @@ __device__ void fold_site4r(const tq_chain& ch, const tq_site& st, int tid, cons
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const C* M = mres + 4 * (oc_lmat(c) + oc_digit(c, al[k], be[k]));
-        const R m0 = M[0].x, m1 = M[1].x, m2 = M[2].x, m3 = M[3].x;
+        R m0, m1, m2, m3;
+        real_factor<R>(M, m0, m1, m2, m3);
         const R n0 = fma(m1, v1[k], m0 * v0[k]);
         const R n1 = fma(m3, v1[k], m2 * v0[k]);
         v0[k] = n0; v1[k] = n1;
@@ -654,8 +675,10 @@ __device__ void ctree_forward(const tq_site& st, int tid, const typename CT<R>::
         const C* M = Mb + 4 * d;
         C n0, n1;
         if constexpr (RE) {   // real path: the complex product's real part, bit for bit
-          n0 = cmk<C>(fma(M[1].x, v1.x, M[0].x * v0.x), R(0));
-          n1 = cmk<C>(fma(M[3].x, v1.x, M[2].x * v0.x), R(0));
+          R m0, m1, m2, m3;
+          real_factor<R>(M, m0, m1, m2, m3);
+          n0 = cmk<C>(fma(m1, v1.x, m0 * v0.x), R(0));
+          n1 = cmk<C>(fma(m3, v1.x, m2 * v0.x), R(0));
         } else {
           n0 = cmul(M[0], v0); cfma(n0, M[1], v1);
           n1 = cmul(M[2], v0); cfma(n1, M[3], v1);
@@ -852,6 +875,56 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
   // computed and each strictly-upper element is stored twice, (i, j) and conj at (j, i).
   // (chi = 32 on the tensor pipe with 3xTF32 mma.sync was measured and reverted: its biased fp32
   // accumulation drifts the norm over long chains, profiles/r02_mma3_tf32_trial.txt)
+#if TQ_RE_HERM44
+  // (CTA only, i.e. LR's Lambda: on RL's P GEMM, CTB, the 4 x 4 tiles measured 0.4% slower)
+  if constexpr (HERM && RE && CTA) {
+    if (LD >= 17 && m == n && n >= 16) {
+      // real path: 4 x 4 tiles (row quad b, column quad c >= b), 36 of 64 at 32 x 32; same
+      // per-element (q, k) order as the 4 x 2 tiles below, so results are identical
+      // (cfg4 LR 4.72 -> 4.57 ms, same-box A/B)
+      const int nb = m >> 2;
+      const int per = nb * (nb + 1) / 2;
+      const int total = ntasks * per;
+      for (int it = tid; it < total; it += TEAM) {
+        const int task = it / per;
+        int r = it - task * per, b = 0;
+        while (r >= nb - b) { r -= nb - b; ++b; }
+        const int i0 = b << 2, j0 = (b + r) << 2;
+        C acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[x][u] = C{0, 0};
+        for (int q = 0; q < nq; ++q) {
+          const C* Ab = fa(task, q) + (CTA ? i0 : i0 * LD);
+          const C* Bb = fb(task, q) + (CTB ? j0 * LD : j0);
+#pragma unroll 4
+          for (int k = 0; k < kk; ++k) {
+            C a[4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bv[u] = CTB ? Bb[u * LD + k] : Bb[k * LD + u];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) a[x] = CTA ? Ab[k * LD + x] : Ab[x * LD + k];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) gmac<RE, 0>(acc[x][u], a[x], bv[u]);
+          }
+        }
+        const C z = {0, 0};
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + x, j = j0 + u;
+            if (j >= i) store(task, i, j, 1, acc[x][u], z, z, z);
+            if (j > i) store(task, j, i, 1, cconj(acc[x][u]), z, z, z);
+          }
+      }
+      return;
+    }
+  }
+#endif
   if constexpr (HERM) {
     if (LD >= 17 && m == n && n >= 16) {
       // 4 rows x 2 adjacent columns per item, tiles (row block b, column pair c) with 2c + 1 >= 4b:
@@ -900,6 +973,50 @@ __device__ __forceinline__ void gemm_group(int tid, int ntasks, int m, int n, in
       return;
     }
   }
+#if TQ_RE_TILE44
+  if constexpr (RE && !CTA && !CTB) {
+    if (LD >= 17 && n >= 16 && m >= 4) {
+      // real path: 4 rows x 4 columns (j + u n/4) per item.  The real FMA chain is smem-bound
+      // (the dead imaginary halves share every wavefront): 8 loads per 16 FMA instead of 6 per 8.
+      // Per output element the (q, k) accumulation order is unchanged, so results are identical.
+      const int qn = n >> 2;
+      const int lqn = 31 - __clz(qn);
+      const int lmb = (31 - __clz(m)) - 2;
+      const int lper = lmb + lqn;
+      const int total = ntasks << lper;
+      for (int it = tid; it < total; it += TEAM) {
+        const int task = it >> lper;
+        const int r = it & ((1 << lper) - 1);
+        const int j = r & (qn - 1);
+        const int i0 = (r >> lqn) << 2;
+        C acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[x][u] = C{0, 0};
+        for (int q = 0; q < nq; ++q) {
+          const C* Ab = fa(task, q) + i0 * LD;
+          const C* Bb = fb(task, q) + j;
+#pragma unroll 4
+          for (int k = 0; k < kk; ++k) {
+            C a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) b[u] = Bb[k * LD + u * qn];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) a[x] = Ab[x * LD + k];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) gmac<RE, 0>(acc[x][u], a[x], b[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) store(task, i0, j + u * qn, 4, acc[0][u], acc[1][u], acc[2][u], acc[3][u]);
+      }
+      return;
+    }
+  }
+#endif
   if (LD >= 17 && n >= 16 && m >= 4) {
     // 4 rows x 2 columns (j, j + n/2) per item: 4 broadcast A loads + 2 B loads per 8 cMAC
     const int hn = n >> 1;
